@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200 hot path on BASELINE.json's headline config.
+
+Workload (BASELINE.json configs[1], "c2"): 268,435,456 uint16 keys, i.i.d. uniform
+over [0, 65535], seed 0, keys-only ascending sort on one B200.  Under torchrun
+(N > 1) every rank sorts its own 2^28-key shard of an N*2^28-key input (global
+indices [r*2^28, (r+1)*2^28)) with the multi-GPU Mode B path: local compressed
+histogram -> NCCL all-reduce of the 512 KiB histogram -> scan -> expansion of the
+rank's own output range (weak scaling).
+
+One step = one pass of the whole hot path (histogram, merge+scan, count-expansion)
+over one batch of input resident in HBM.  Inputs (512 MiB) are larger than L2
+(126 MB), so no flush is needed between steps.  Timing: CUDA events recorded by
+the library at its phase boundaries (fs_set_phase_events) on the launching
+stream, W untimed warm-up steps, exactly K timed steps bracketed by barrier +
+synchronize, max over ranks.
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (the
+"reference arm" of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gkeys/s and achieved HBM GB/s (% of roofline) at 1/2/4/8 B200"
+N_PER_GPU = 1 << 28
+WORKLOAD = "c2: 268,435,456 uint16 keys per GPU, i.i.d. uniform [0,65535], seed 0, keys-only ascending sort"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="fs", choices=["fs", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default: config c2)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ peaks and clocks
+def measured_peak_gbs():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: b.copy_ read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons through NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        reasons = [name for bit, name in REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML polled every ~2 ms during the timed region"}
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def time_oracle(n_sample: int, steps: int, warmup: int, min_seconds: float = 0.0):
+    """The oracle as it stands (single-threaded C counting sort) on a bounded sample."""
+    import numpy as np  # noqa: F401
+
+    import datagen
+    import oracle
+    keys = datagen.gen_u16("uniform", n_sample, seed=0, n_total=N_PER_GPU)
+    for _ in range(warmup):
+        oracle.sort_u16(keys)
+    reps, t0 = 0, time.perf_counter()
+    while reps < steps or (time.perf_counter() - t0) < min_seconds:
+        out = oracle.sort_u16(keys)
+        reps += 1
+    dt = time.perf_counter() - t0
+    ok = bool((out[1:] >= out[:-1]).all())
+    return n_sample * reps / dt / 1e9, reps, dt, ok
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_sample = 1 << 26
+    v, reps, dt, ok = time_oracle(n_sample, args.steps, args.warmup)
+    sample = f"first 2^26 keys of the c2 input per step (1/4 of the 2^28-key workload), {reps} steps"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Gkeys/s", "n_gpus": args.gpus,
+        "steps": reps, "warmup": args.warmup, "ms_per_step": round(dt / reps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "reference": "CPU oracle (oracle/oracle.c counting sort), single thread"},
+        "cpu_baseline": {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model(), "host_cores": host_cores()},
+        "e2e": {"value": round(v, 6), "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "verified_nondecreasing": ok,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def load_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
+            os.path.join(ROOT, "profiles")) else []:
+        if name.startswith("ncu_traffic") and name.endswith(".json"):
+            try:
+                d = json.load(open(os.path.join(ROOT, "profiles", name)))
+                if kernel in d:
+                    return d[kernel].get("dram_bytes_per_launch"), name
+            except Exception:
+                pass
+    return None, None
+
+
+def run_fs(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import datagen
+    import paper_2605_10390_b200 as fs
+    from paper_2605_10390_b200 import _lib
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L = fs.lib()
+    n = args.n
+    n_total = n * world
+    i0 = rank * n
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+
+    keys = torch.empty(n, dtype=torch.uint16, device=dev)
+    datagen.gen_u16_device(keys.data_ptr(), "uniform", n, seed=0, i0=i0, n_total=n_total, stream=s)
+    out = torch.empty(n, dtype=torch.uint16, device=dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        hist = torch.empty(65536, dtype=torch.int64, device=dev)
+        prefix = torch.empty(65537, dtype=torch.int64, device=dev)
+        htemp = torch.empty(L.fs_histogram_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
+        stemp = torch.empty(L.fs_exclusive_scan_u64_temp_bytes(65536), dtype=torch.uint8, device=dev)
+        b0, b1 = (n_total * rank) // world, (n_total * (rank + 1)) // world
+    else:
+        temp = torch.empty(L.fs_sort_keys_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
+    nev = 4 if world == 1 else 5
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    for row in events:
+        for e in row:
+            e.record(stream)  # materialise the cudaEvent_t handles
+    handles = [(ctypes_array(row)) for row in events]
+    torch.cuda.synchronize()
+
+    def step(ev_row=None, ev_handles=None):
+        if world == 1:
+            if ev_handles is not None:
+                L.fs_set_phase_events(ev_handles, nev)
+            _lib.check(L.fs_sort_keys_u16(keys.data_ptr(), out.data_ptr(), n, 16, temp.data_ptr(), temp.numel(), s),
+                       "fs_sort_keys_u16")
+            if ev_handles is not None:
+                L.fs_set_phase_events(None, 0)
+        else:
+            if ev_row is not None:
+                ev_row[0].record(stream)
+            _lib.check(L.fs_histogram_u16(keys.data_ptr(), n, 16, hist.data_ptr(), 0, htemp.data_ptr(),
+                                          htemp.numel(), s), "fs_histogram_u16")
+            if ev_row is not None:
+                ev_row[1].record(stream)
+            dist.all_reduce(hist)  # NCCL, 512 KiB: the global histogram merge across GPUs
+            if ev_row is not None:
+                ev_row[2].record(stream)
+            _lib.check(L.fs_exclusive_scan_u64(hist.data_ptr(), prefix.data_ptr(), 65536, stemp.data_ptr(),
+                                               stemp.numel(), s), "fs_exclusive_scan_u64")
+            if ev_row is not None:
+                ev_row[3].record(stream)
+            _lib.check(L.fs_expand_u16(prefix.data_ptr(), 65536, b0, b1, out.data_ptr(), s), "fs_expand_u16")
+            if ev_row is not None:
+                ev_row[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        for k in range(args.steps):
+            step(events[k], handles[k])
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    total_ms = events[0][0].elapsed_time(events[-1][nev - 1])
+    phase_ms = [statistics.mean(row[i].elapsed_time(row[i + 1]) for row in events) for i in range(nev - 1)]
+    t_max = total_ms
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    value = n_total * args.steps / (t_max * 1e-3) / 1e9
+
+    # Roofline of the dominant kernel (algorithmic bytes = 2 B/key read for the
+    # histogram, 2 B/key written for the expansion).
+    if world == 1:
+        names = {"hist16": phase_ms[0], "expand16": phase_ms[2]}
+        scan_ms = phase_ms[1]
+    else:
+        names = {"hist16+merge": phase_ms[0], "expand16": phase_ms[3]}
+        scan_ms = phase_ms[2]
+    dom = max(names, key=names.get)
+    dom_ms = names[dom]
+    alg_bytes = 2 * (n if world == 1 else (b1 - b0) if dom == "expand16" else n)
+    peak, peak_src = measured_peak_gbs()
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic(dom.split("+")[0])
+    whole_bytes = 4 * n
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": WORKLOAD if n == N_PER_GPU else f"{n} uint16 keys per GPU, uniform, seed 0",
+                   "keys_per_gpu": n, "keys_total": n_total, "parallelism": f"dp{world}",
+                   "multi_gpu_mode": None if world == 1 else "B (histogram all-reduce + own-range expansion)",
+                   "l2": "inputs (512 MiB/GPU) larger than L2 (126 MB): no flush between steps"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(dom_ms, 5),
+                     "peak_source": peak_src, "traffic_source": traffic_src},
+        "whole_step": {"algorithmic_bytes": whole_bytes, "achieved_GBps": round(whole_bytes / (t_max / args.steps * 1e-3) / 1e9, 1),
+                       "frac_of_measured_peak": round(whole_bytes / (t_max / args.steps * 1e-3) / 1e9 / peak, 4),
+                       "frac_of_8TBps": round(whole_bytes / (t_max / args.steps * 1e-3) / 8e12, 4)},
+        "phases_ms": {k: round(v, 5) for k, v in zip(
+            (["hist16", "merge_scan", "expand16"] if world == 1 else ["hist16+merge", "nccl_allreduce", "scan", "expand16"]),
+            phase_ms)},
+        "gpu_launches": (3 if world == 1 else 4) * args.steps,
+        "clocks": clocks.summary(),
+    }
+    del scan_ms
+
+    # End to end through the public host-buffer API: H2D of the step's keys from
+    # pinned memory, the sort, D2H of the sorted keys, every step.
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, L, _lib, keys, n, n_total, rank, world, dev, dist)
+
+    if not args.no_verify and world == 1:
+        line["verified"] = verify(out, keys)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, reps, dt, ok = time_oracle(n, 3, 0, min_seconds=10.0)
+        line["cpu_baseline"] = {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+                                "sample": f"the full c2 input (2^28 keys) sorted {reps} times ({dt:.1f} s) by the "
+                                          f"single-threaded C oracle", "cpu": cpu_model(), "host_cores": host_cores()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ctypes_array(events):
+    import ctypes
+    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    return arr
+
+
+def e2e(args, L, _lib, keys, n, n_total, rank, world, dev, dist):
+    import torch
+    steps = max(1, min(args.steps, 5))
+    host_in = keys.cpu().pin_memory()
+    host_out = torch.empty(n, dtype=torch.uint16).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+    if world == 1:
+        work = torch.empty(L.fs_sort_keys_u16_host_work_bytes(n, 0), dtype=torch.uint8, device=dev)
+
+        def one():
+            _lib.check(L.fs_sort_keys_u16_host(host_in.data_ptr(), host_out.data_ptr(), n, 0, work.data_ptr(),
+                                               work.numel(), s), "fs_sort_keys_u16_host")
+        h2d, d2h = 2 * n, 2 * n
+    else:
+        d_in = torch.empty(n, dtype=torch.uint16, device=dev)
+        d_out = torch.empty(n, dtype=torch.uint16, device=dev)
+        hist = torch.empty(65536, dtype=torch.int64, device=dev)
+        prefix = torch.empty(65537, dtype=torch.int64, device=dev)
+        htemp = torch.empty(L.fs_histogram_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
+        stemp = torch.empty(L.fs_exclusive_scan_u64_temp_bytes(65536), dtype=torch.uint8, device=dev)
+        b0, b1 = (n_total * rank) // world, (n_total * (rank + 1)) // world
+
+        def one():
+            d_in.copy_(host_in, non_blocking=True)
+            _lib.check(L.fs_histogram_u16(d_in.data_ptr(), n, 16, hist.data_ptr(), 0, htemp.data_ptr(),
+                                          htemp.numel(), s), "fs_histogram_u16")
+            dist.all_reduce(hist)
+            _lib.check(L.fs_exclusive_scan_u64(hist.data_ptr(), prefix.data_ptr(), 65536, stemp.data_ptr(),
+                                               stemp.numel(), s), "fs_exclusive_scan_u64")
+            _lib.check(L.fs_expand_u16(prefix.data_ptr(), 65536, b0, b1, d_out.data_ptr(), s), "fs_expand_u16")
+            host_out[:b1 - b0].copy_(d_out[:b1 - b0], non_blocking=True)
+        h2d, d2h = 2 * n, 2 * (b1 - b0)
+    one()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(n_total * steps / (ms * 1e-3) / 1e9, 4), "unit": "Gkeys/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "api": "fs_sort_keys_u16_host (pinned host buffers, batched copy/compute overlap)" if world == 1
+            else "H2D + fs_histogram_u16 + NCCL all_reduce + fs_exclusive_scan_u64 + fs_expand_u16 + D2H"}
+
+
+def verify(out, keys):
+    """Cheap end check of the timed output against the oracle (rank 0, N = 1)."""
+    import numpy as np
+
+    import oracle
+    k = keys.cpu().numpy()
+    o = out.cpu().numpy()
+    return bool(np.array_equal(o, oracle.sort_u16(k)))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import datetime
+
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", timeout=datetime.timedelta(seconds=600),
+                                device_id=torch.device("cuda", local_rank))
+    try:
+        run_fs(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * fractalsort.h — C ABI of libfractalsort.so, the B200-native (sm_100a) hot path
+ * of FractalSortCPU (arXiv 2605.10390): histogram-driven radix sorting of
+ * fixed-width unsigned keys with the paper's compressed histogram.
+ *
+ * Citations are lines of /root/reference/PAPER.md (section named) and of SPEC.md;
+ * readings of ambiguous passages are the ledger items of SURVEY.md §8(c).3, listed
+ * in DESIGN.md §Readings.
+ *
+ * Problem statement: sort n keys of precision p = key_bits
+ * ascending; the output is the "Sorted array K of n reconstructed p-bit keys"
+ * (Alg. 5).  For key/value pairs the sort is stable: values are the
+ * paper's index array I, which "maps each sorted position to an arrival position"
+ * (ledger 13).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Pointers named keys/vals/hist/prefix/out/temp are DEVICE pointers (CUDA
+ *    global memory of the current device), except where a name ends in _host.
+ *    The caller owns every buffer; the library allocates nothing on the hot path
+ *    and keeps no state except a per-device attribute cache (thread-safe).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    asynchronous and stream-ordered; there is no host synchronisation, so
+ *    device-side faults surface at the caller's next synchronisation.  Setting
+ *    the environment variable FS_SYNC_CHECK=1 makes every call synchronise and
+ *    report asynchronous errors as FS_ERR_CUDA (debugging aid).
+ *  - n is a 64-bit element count (up to 2^34 per device is exercised); all
+ *    counts and positions are 64-bit.
+ *  - n == 0 returns FS_OK without launching anything (ledger 14).
+ *  - key_bits: 0 means the full key width; otherwise 1..width.  Keys must be
+ *    < 2^key_bits ("key < 2^p"); violating that is a precondition
+ *    error with unspecified (but memory-safe) output.  For u16 keys-only the
+ *    output is the exact sort even then; key_bits only sets hist sizes.
+ *  - Errors are returned, never printed or aborted on: NULL pointers with n > 0,
+ *    temp_bytes smaller than the matching *_temp_bytes(), key_bits out of range,
+ *    or forbidden aliasing give FS_ERR_INVALID_ARGUMENT before any CUDA call;
+ *    launch failures give FS_ERR_CUDA.  fs_last_error_message() holds a
+ *    thread-local detail string for the last failure on the calling thread.
+ *  - Results are deterministic and bit-identical across runs, grid sizes and
+ *    devices (integer arithmetic only; stability fixes the order of equal keys).
+ *  - temp must be 256-byte aligned (torch / cudaMalloc allocations are).
+ */
+#ifndef FRACTALSORT_H
+#define FRACTALSORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fs_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FS_OK = 0,
+  FS_ERR_INVALID_ARGUMENT = 1,
+  FS_ERR_CUDA = 2,
+  FS_ERR_OUT_OF_MEMORY = 3,
+  FS_ERR_UNSUPPORTED = 4
+} fs_status;
+
+/* Static English name of a status code. */
+const char* fs_status_string(fs_status s);
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+const char* fs_last_error_message(void);
+/* ABI version: (major << 16) | minor. */
+int fs_version(void);
+
+/* ----------------------------------------------------------------------------
+ * Temp sizing.  Each returns the minimum temp_bytes for the matching call with
+ * the same arguments on the current device (depends on the SM count).
+ * ------------------------------------------------------------------------- */
+size_t fs_sort_keys_u16_temp_bytes(uint64_t n);
+size_t fs_sort_keys_u32_temp_bytes(uint64_t n, int key_bits);
+size_t fs_sort_keys_u64_temp_bytes(uint64_t n, int key_bits);
+size_t fs_sort_pairs_u64_u32_temp_bytes(uint64_t n, int key_bits);
+size_t fs_histogram_u16_temp_bytes(uint64_t n);
+size_t fs_exclusive_scan_u64_temp_bytes(uint64_t nbins);
+
+/* ----------------------------------------------------------------------------
+ * fs_sort_keys_u16 — keys-only ascending sort of n u16 keys (configs c1-c4).
+ *
+ * The three stages of the paper's method at p = 16, n > 2^p (the full-histogram
+ * branch, §III.G; K1 of SURVEY.md §0.3):
+ *   1. compressed histogram of the 65,536 leaf bins: every key increments the
+ *      leaf its MSB-first bit path selects (Fractal RMW, §III.B.1;
+ *      Alg. 1), in 16-bit tapered counters packed two per
+ *      32-bit word (§III.D.1, 197 §III.F.1, n_L = W/w_c PAPER.md:222),
+ *      per-SM local trees merged into one global histogram;
+ *   2. exclusive scan P[v] = #keys < v = GetIndex(v) for all v (Alg. 3,
+ *      PAPER.md:168-190);
+ *   3. reconstruction = count-expansion: out[P[v] .. P[v+1]) = v (Alg. 5,
+ *      PAPER.md:256-286, with t = 0 and l_b = 0).
+ * keys_in, keys_out: device arrays of n u16.  keys_out == keys_in (in place) is
+ * allowed; any other overlap is FS_ERR_INVALID_ARGUMENT.  key_bits: 0 or 1..16.
+ * temp: >= fs_sort_keys_u16_temp_bytes(n) device bytes (contents undefined on
+ * entry and exit).
+ * ------------------------------------------------------------------------- */
+fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t n, int key_bits, void* temp,
+                           size_t temp_bytes, fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * fs_sort_keys_u32 / fs_sort_keys_u64 — keys-only ascending sort of wider keys:
+ * stable LSD radix ("histogram, prefix sum and stable scatter phases",
+ * PAPER.md:52 §II) with 8-bit digits and one compressed histogram per digit,
+ * all digit histograms computed in one read pass (config c5's "multi-digit
+ * precision scaling with compressed histograms per digit", ledger 25).
+ * ceil(key_bits / 8) scatter passes; a digit whose histogram has one non-empty
+ * bin is skipped.  keys_in and keys_out must not overlap.  key_bits: 0 or
+ * 1..32 (u32), 0 or 1..64 (u64).
+ * ------------------------------------------------------------------------- */
+fs_status fs_sort_keys_u32(const uint32_t* keys_in, uint32_t* keys_out, uint64_t n, int key_bits, void* temp,
+                           size_t temp_bytes, fs_stream_t stream);
+fs_status fs_sort_keys_u64(const uint64_t* keys_in, uint64_t* keys_out, uint64_t n, int key_bits, void* temp,
+                           size_t temp_bytes, fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * fs_sort_pairs_u64_u32 — STABLE ascending sort of (u64 key, u32 value) pairs
+ * by key (config c5).  Equal keys keep their input order, so with
+ * vals_in[i] = i the output values are Alg. 5's index array I.
+ * Same LSD scheme as fs_sort_keys_u64; keys and values move together.
+ * No input buffer may overlap an output buffer.
+ * ------------------------------------------------------------------------- */
+fs_status fs_sort_pairs_u64_u32(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
+                                uint32_t* vals_out, uint64_t n, int key_bits, void* temp, size_t temp_bytes,
+                                fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Phase API (batch streaming with histogram reuse, and the multi-GPU driver).
+ *
+ * fs_histogram_u16: hist[v] (+)= #{i : keys[i] == v} for v < 2^key_bits (device
+ * u64 array of 2^key_bits entries).  accumulate = 1 adds to the existing hist —
+ * the "cached histogram from a terminating batch is reused by the next batch"
+ * of Batch Counter Update (§III.D); accumulate = 0 overwrites.
+ * hist may be reinterpreted by the caller as int64 (counts < 2^63).
+ * ------------------------------------------------------------------------- */
+fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint64_t* hist, int accumulate,
+                           void* temp, size_t temp_bytes, fs_stream_t stream);
+
+/* fs_exclusive_scan_u64: prefix[v] = sum_{u<v} hist[u] for v = 0..nbins, so
+ * prefix[nbins] is the total (Alg. 3 GetIndex for every v).
+ * hist: nbins u64; prefix: nbins + 1 u64; they must not overlap.  Single-pass
+ * decoupled-lookback scan.  nbins >= 1; runs even for a zero total. */
+fs_status fs_exclusive_scan_u64(const uint64_t* hist, uint64_t* prefix, uint64_t nbins, void* temp,
+                                size_t temp_bytes, fs_stream_t stream);
+
+/* fs_expand_u16: count-expansion of a prefix array (Alg. 5 with t = 0, l_b = 0,
+ * PAPER.md:259-284): writes the keys at global sorted positions
+ * [out_begin, out_end) to out[0 .. out_end - out_begin), where the key at
+ * position j is the v with prefix[v] <= j < prefix[v+1].  prefix: nbins + 1
+ * non-decreasing u64 (nbins <= 65536) with out_end <= prefix[nbins].
+ * This is how a rank of the multi-GPU path writes its own output range
+ * (SURVEY.md §8(e) Mode B).  No temp needed. */
+fs_status fs_expand_u16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
+                        uint16_t* out, fs_stream_t stream);
+
+/* fs_send_counts: multi-GPU payload exchange plan (SURVEY.md §8(e) Mode A,
+ * ledger 13, 23).  hist_all: G x nbins u64 (row r = rank r's histogram, as
+ * gathered).  Rank d owns global sorted positions [floor(d*N/G),
+ * floor((d+1)*N/G)), N = total; rank g's keys of value v occupy positions
+ * [P[v] + S_<g[v], P[v] + S_<=g[v]) (lower rank first).  Writes
+ * send[d] = number of rank g's keys that land in rank d's range (G u64, device).
+ * G in 1..1024, 0 <= g < G, nbins <= 65536. */
+fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
+                         fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Host-buffer entry point (end-to-end use, and the out-of-core path of Batch
+ * Size Selection / Batch Counter Update): sorts n u16 keys
+ * that live in HOST memory into a host output array.  The input streams to the
+ * device in batches of `batch` keys, each histogrammed into one reused
+ * histogram as it lands (copy of batch i+1 overlaps the histogram of batch i);
+ * then the output is expanded batch by batch and streamed back (expansion of
+ * batch j+1 overlaps the copy-out of batch j).  keys_in_host / keys_out_host
+ * should be page-locked for full PCIe/C2C overlap (pageable memory works but
+ * serialises copies).  work: device workspace of
+ * fs_sort_keys_u16_host_work_bytes(n, batch) bytes.  batch = 0 picks a default.
+ * The call returns when the work is enqueued; synchronise `stream` before
+ * reading keys_out_host.
+ * ------------------------------------------------------------------------- */
+size_t fs_sort_keys_u16_host_work_bytes(uint64_t n, uint64_t batch);
+fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out_host, uint64_t n,
+                                uint64_t batch, void* work, size_t work_bytes, fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
+ * Phase instrumentation (measurement).  events: array of
+ * `count` cudaEvent_t handles (created by the caller), or NULL to disable.
+ * While set, the sort calls made on THIS thread record events[i] on their
+ * stream at phase boundaries, i < count:
+ *   fs_sort_keys_u16:  [0] start, [1] after the histogram kernel, [2] after the
+ *                      merge+scan kernel, [3] after the expansion kernel;
+ *   wide sorts:        [0] start, [1] after the digit histograms + plan,
+ *                      [2 + p] after scatter pass p (passes ceil(key_bits/8)),
+ *                      last after the identity copy check.
+ * The library does not own or destroy the events.  Returns FS_OK.
+ * ------------------------------------------------------------------------- */
+fs_status fs_set_phase_events(void* const* events, int count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRACTALSORT_H */

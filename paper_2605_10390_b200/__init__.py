@@ -1,0 +1,191 @@
+"""paper_2605_10390_b200 — B200-native compressed-histogram radix sort (FractalSortCPU,
+arXiv 2605.10390), as a thin Python binding over libfractalsort.so.
+
+Every step of the sort runs in the library's sm_100a kernels; this module only
+marshals arguments: it allocates outputs and temp buffers with torch, passes raw
+device pointers and the current CUDA stream to the C ABI (include/fractalsort.h)
+and raises on a non-OK status.  There is no CPU fallback: CPU tensors raise.
+
+Names follow the C ABI: sort_keys (fs_sort_keys_u16/u32/u64), sort_pairs
+(fs_sort_pairs_u64_u32), histogram_u16 / exclusive_scan / expand_u16 (the phase
+API), send_counts (multi-GPU exchange plan) and sort_keys_u16_host (host
+buffers, streamed in batches).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import FractalSortError, check, lib
+
+__all__ = [
+    "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
+    "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
+]
+
+_TEMP_ALIGN = 256
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor) -> torch.device:
+    dev = ts[0].device
+    for t in ts:
+        if t.device.type != "cuda":
+            raise ValueError("paper_2605_10390_b200 runs on CUDA tensors only (no CPU fallback)")
+        if t.device != dev:
+            raise ValueError("all tensors must be on the same device")
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+    return dev
+
+
+def _temp(nbytes: int, device: torch.device) -> torch.Tensor:
+    # torch's caching allocator returns >= 512-byte aligned blocks.
+    t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    assert t.data_ptr() % _TEMP_ALIGN == 0
+    return t
+
+
+def sort_keys(keys: torch.Tensor, key_bits: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Ascending keys-only sort of a 1-D uint16/uint32/uint64 CUDA tensor.
+
+    uint16 -> fs_sort_keys_u16 (histogram, scan, count-expansion; out may be keys);
+    uint32/uint64 -> fs_sort_keys_u32/u64 (LSD with one compressed histogram per digit).
+    """
+    dev = _require_cuda(keys)
+    n = keys.numel()
+    if out is None:
+        out = torch.empty_like(keys)
+    else:
+        _require_cuda(out)
+        if out.dtype != keys.dtype or out.numel() != n:
+            raise ValueError("out must match keys in dtype and size")
+    L = lib()
+    with torch.cuda.device(dev):
+        s = _stream(dev)
+        if keys.dtype == torch.uint16:
+            temp = _temp(L.fs_sort_keys_u16_temp_bytes(n), dev)
+            check(L.fs_sort_keys_u16(keys.data_ptr(), out.data_ptr(), n, key_bits, temp.data_ptr(),
+                                     temp.numel(), s), "fs_sort_keys_u16")
+        elif keys.dtype == torch.uint32:
+            temp = _temp(L.fs_sort_keys_u32_temp_bytes(n, key_bits), dev)
+            check(L.fs_sort_keys_u32(keys.data_ptr(), out.data_ptr(), n, key_bits, temp.data_ptr(),
+                                     temp.numel(), s), "fs_sort_keys_u32")
+        elif keys.dtype == torch.uint64:
+            temp = _temp(L.fs_sort_keys_u64_temp_bytes(n, key_bits), dev)
+            check(L.fs_sort_keys_u64(keys.data_ptr(), out.data_ptr(), n, key_bits, temp.data_ptr(),
+                                     temp.numel(), s), "fs_sort_keys_u64")
+        else:
+            raise TypeError(f"unsupported key dtype {keys.dtype}")
+    return out
+
+
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, key_bits: int = 0):
+    """Stable ascending sort of (uint64 key, uint32 value) pairs by key (fs_sort_pairs_u64_u32)."""
+    dev = _require_cuda(keys, vals)
+    if keys.dtype != torch.uint64 or vals.dtype != torch.uint32 or keys.numel() != vals.numel():
+        raise TypeError("sort_pairs expects uint64 keys and uint32 values of equal length")
+    n = keys.numel()
+    ko, vo = torch.empty_like(keys), torch.empty_like(vals)
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_sort_pairs_u64_u32_temp_bytes(n, key_bits), dev)
+        check(L.fs_sort_pairs_u64_u32(keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(), n,
+                                      key_bits, temp.data_ptr(), temp.numel(), _stream(dev)),
+              "fs_sort_pairs_u64_u32")
+    return ko, vo
+
+
+def histogram_u16(keys: torch.Tensor, key_bits: int = 16, hist: torch.Tensor | None = None,
+                  accumulate: bool = False) -> torch.Tensor:
+    """hist[v] (+)= #{i: keys[i] == v} (fs_histogram_u16); hist is int64 (bit-identical to u64)."""
+    dev = _require_cuda(keys)
+    if keys.dtype != torch.uint16:
+        raise TypeError("histogram_u16 expects uint16 keys")
+    nb = 1 << (key_bits or 16)
+    if hist is None:
+        hist = torch.empty(nb, dtype=torch.int64, device=dev)
+        accumulate = False
+    elif hist.numel() != nb or hist.dtype not in (torch.int64, torch.uint64):
+        raise ValueError("hist must hold 2^key_bits int64/uint64 counters")
+    n = keys.numel()
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_histogram_u16_temp_bytes(n), dev)
+        check(L.fs_histogram_u16(keys.data_ptr(), n, key_bits, hist.data_ptr(), int(bool(accumulate)),
+                                 temp.data_ptr(), temp.numel(), _stream(dev)), "fs_histogram_u16")
+    return hist
+
+
+def exclusive_scan(hist: torch.Tensor) -> torch.Tensor:
+    """prefix[v] = sum_{u<v} hist[u], prefix[nbins] = total (fs_exclusive_scan_u64)."""
+    dev = _require_cuda(hist)
+    if hist.dtype not in (torch.int64, torch.uint64):
+        raise TypeError("exclusive_scan expects int64/uint64 counts")
+    nb = hist.numel()
+    prefix = torch.empty(nb + 1, dtype=hist.dtype, device=dev)
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_exclusive_scan_u64_temp_bytes(nb), dev)
+        check(L.fs_exclusive_scan_u64(hist.data_ptr(), prefix.data_ptr(), nb, temp.data_ptr(), temp.numel(),
+                                      _stream(dev)), "fs_exclusive_scan_u64")
+    return prefix
+
+
+def expand_u16(prefix: torch.Tensor, out_begin: int, out_end: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Keys at global sorted positions [out_begin, out_end) from a prefix array (fs_expand_u16)."""
+    dev = _require_cuda(prefix)
+    n = out_end - out_begin
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint16, device=dev)
+    elif out.dtype != torch.uint16 or out.numel() < n:
+        raise ValueError("out must be uint16 with room for out_end - out_begin keys")
+    with torch.cuda.device(dev):
+        check(lib().fs_expand_u16(prefix.data_ptr(), prefix.numel() - 1, out_begin, out_end, out.data_ptr(),
+                                  _stream(dev)), "fs_expand_u16")
+    return out
+
+
+def send_counts(hist_all: torch.Tensor, g: int) -> torch.Tensor:
+    """send[d] = how many of rank g's keys land in rank d's output range (fs_send_counts)."""
+    dev = _require_cuda(hist_all)
+    G, nb = hist_all.shape
+    send = torch.empty(G, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_send_counts(hist_all.data_ptr(), G, g, nb, send.data_ptr(), _stream(dev)),
+              "fs_send_counts")
+    return send
+
+
+def sort_keys_u16_host_work_bytes(n: int, batch: int = 0) -> int:
+    return int(lib().fs_sort_keys_u16_host_work_bytes(n, batch))
+
+
+def sort_keys_u16_host(keys_host: torch.Tensor, out_host: torch.Tensor | None = None, batch: int = 0,
+                       device: torch.device | int | None = None, work: torch.Tensor | None = None,
+                       synchronize: bool = True) -> torch.Tensor:
+    """Sort host-resident uint16 keys into a host tensor through the device (fs_sort_keys_u16_host).
+
+    Pass pinned tensors (``tensor.pin_memory()``) for overlapped copies.
+    """
+    if keys_host.device.type != "cpu" or keys_host.dtype != torch.uint16 or not keys_host.is_contiguous():
+        raise ValueError("keys_host must be a contiguous uint16 CPU tensor")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       (device if isinstance(device, int) else device.index or 0))
+    n = keys_host.numel()
+    if out_host is None:
+        out_host = torch.empty(n, dtype=torch.uint16, pin_memory=keys_host.is_pinned())
+    L = lib()
+    with torch.cuda.device(dev):
+        need = L.fs_sort_keys_u16_host_work_bytes(n, batch)
+        if work is None or work.numel() < need:
+            work = _temp(need, dev)
+        s = _stream(dev)
+        check(L.fs_sort_keys_u16_host(keys_host.data_ptr(), out_host.data_ptr(), n, batch, work.data_ptr(),
+                                      work.numel(), s), "fs_sort_keys_u16_host")
+        if synchronize:
+            torch.cuda.current_stream(dev).synchronize()
+    return out_host

@@ -1,0 +1,56 @@
+// kernels.cuh — internal launch interface between the C ABI (abi.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fs {
+
+struct DeviceInfo {
+  int device = 0;
+  int sm_count = 0;
+  int max_smem_optin = 0;
+  int l2_bytes = 0;
+  int cc_major = 0, cc_minor = 0;
+};
+// Cached per device, initialised thread-safely on first use (abi.cu).
+const DeviceInfo& device_info();
+
+// ---------------------------------------------------------------- hist16.cu
+// Per-SM compressed histogram of u16 keys (stage 1).  One CTA per SM.
+constexpr int kHistBins = 65536;
+constexpr int kHistWords = kHistBins / 2;  // two 16-bit counters per 32-bit word
+int hist16_grid(uint64_t n);
+// partials: grid x kHistWords packed words; spill: 65536 u64, must be zero on entry.
+cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill,
+                          int grid, cudaStream_t s);
+
+// ---------------------------------------------------------------- scan.cu
+constexpr int kScanTileBins = 256;
+inline uint64_t scan_tiles(uint64_t nbins) { return (nbins + kScanTileBins - 1) / kScanTileBins; }
+// Merge + scan (stages 1b+2).  Source is either the packed per-SM partials plus
+// spill (hist_in == nullptr) or a u64 histogram.  hist_out: nullptr, or written
+// (accumulate = 0) / added to (accumulate = 1) for v < nbins_out.  prefix:
+// nullptr (merge only) or nbins + 1 entries.  status (scan_tiles(nbins) u64)
+// and *ticket must be zero on entry when prefix != nullptr.
+cudaError_t launch_merge_scan(const uint32_t* partials, int parts, const unsigned long long* spill,
+                              const uint64_t* hist_in, uint64_t nbins, uint64_t* hist_out, uint64_t nbins_out,
+                              int accumulate, uint64_t* prefix, unsigned long long* status, uint32_t* ticket,
+                              cudaStream_t s);
+
+// ---------------------------------------------------------------- expand16.cu
+// Count-expansion of prefix into out for global positions [out_begin, out_end) (stage 3).
+cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
+                            uint16_t* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- partition.cu
+cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
+                               cudaStream_t s);
+
+// ---------------------------------------------------------------- onesweep.cu
+// LSD radix sort of u32/u64 keys (+ optional u32 values), 8-bit digits.
+size_t onesweep_temp_bytes(uint64_t n, int key_bytes, int key_bits, bool has_values);
+cudaError_t onesweep_sort(const void* keys_in, const uint32_t* vals_in, void* keys_out, uint32_t* vals_out,
+                          uint64_t n, int key_bytes, int key_bits, void* temp, size_t temp_bytes,
+                          cudaStream_t s);
+
+}  // namespace fs

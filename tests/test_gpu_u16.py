@@ -1,0 +1,188 @@
+"""GPU parity of the u16 hot path (histogram -> scan -> count-expansion) against the
+CPU oracle, through the C ABI (via the thin binding).  Bar: bit-exact (integer work).
+
+Sizes span several tiles and ragged tails; full-size configs c1-c3 of BASELINE.json
+are compared element by element in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+import paper_2605_10390_b200 as fs
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(a: np.ndarray, dev) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+EDGE_N = [1, 2, 7, 8, 9, 31, 32, 33, 255, 4097, 65535, 65536, 65537, 131071, (1 << 20) + 7, 3_000_001]
+
+
+@pytest.mark.parametrize("n", EDGE_N)
+def test_sort_u16_uniform_edges(cuda, n):
+    keys = datagen.gen_u16("uniform", n, seed=n)
+    out = fs.sort_keys(to_dev(keys, cuda))
+    np.testing.assert_array_equal(to_host(out), oracle.sort_u16(keys))
+
+
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "gauss", "sortedswap", "const"])
+@pytest.mark.parametrize("n", [1000, 65536 * 3 + 5, 1 << 21])
+def test_sort_u16_distributions(cuda, dist, n):
+    keys = datagen.gen_u16(dist, n, seed=7)
+    out = fs.sort_keys(to_dev(keys, cuda))
+    np.testing.assert_array_equal(to_host(out), oracle.sort_u16(keys))
+
+
+@pytest.mark.parametrize("value", [0, 1, 0xA5A5, 65534, 65535])
+def test_sort_u16_all_equal(cuda, value):
+    n = (1 << 22) + 3  # forces many spills of one hot counter per SM
+    keys = np.full(n, value, dtype=np.uint16)
+    out = to_host(fs.sort_keys(to_dev(keys, cuda)))
+    np.testing.assert_array_equal(out, keys)
+
+
+def test_sort_u16_two_hot_bins(cuda):
+    """Adversarial for the 16-bit packed counters: both halves of one word are hot."""
+    n = 1 << 23
+    rng = np.random.default_rng(3)
+    keys = rng.choice(np.array([4242, 4243], dtype=np.uint16), size=n)
+    out = to_host(fs.sort_keys(to_dev(keys, cuda)))
+    np.testing.assert_array_equal(out, oracle.sort_u16(keys))
+
+
+@pytest.mark.parametrize("offset", range(8))
+def test_sort_u16_misaligned(cuda, offset):
+    """Input and output start at every 2-byte offset of a 16-byte vector."""
+    n = 100_003
+    keys = datagen.gen_u16("uniform", n + 16, seed=11)
+    src = to_dev(keys, cuda)[offset:offset + n]
+    dst_buf = torch.empty(n + 16, dtype=torch.uint16, device=cuda)
+    dst = dst_buf[(7 * offset) % 8:(7 * offset) % 8 + n]
+    fs.sort_keys(src, out=dst)
+    np.testing.assert_array_equal(to_host(dst), oracle.sort_u16(keys[offset:offset + n]))
+
+
+def test_sort_u16_in_place(cuda):
+    keys = datagen.gen_u16("zipf", 1 << 20, seed=5)
+    t = to_dev(keys, cuda)
+    fs.sort_keys(t, out=t)
+    np.testing.assert_array_equal(to_host(t), oracle.sort_u16(keys))
+
+
+def test_sort_u16_empty(cuda):
+    t = torch.empty(0, dtype=torch.uint16, device=cuda)
+    assert fs.sort_keys(t).numel() == 0
+
+
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "gauss", "sortedswap", "const"])
+def test_histogram_u16(cuda, dist):
+    keys = datagen.gen_u16(dist, 5_000_017, seed=2)
+    h = to_host(fs.histogram_u16(to_dev(keys, cuda))).astype(np.uint64)
+    np.testing.assert_array_equal(h, oracle.histogram_u16(keys))
+
+
+def test_histogram_u16_accumulate_and_key_bits(cuda):
+    a = datagen.gen_u16("uniform", 300_000, seed=1, key_bits=12)
+    b = datagen.gen_u16("uniform", 200_001, seed=2, key_bits=12)
+    h = fs.histogram_u16(to_dev(a, cuda), key_bits=12)
+    fs.histogram_u16(to_dev(b, cuda), key_bits=12, hist=h, accumulate=True)
+    want = oracle.histogram_u16(np.concatenate([a, b]))[:4096]
+    np.testing.assert_array_equal(to_host(h).astype(np.uint64), want)
+    # n = 0 with accumulate = 0 zeroes the histogram
+    fs.histogram_u16(torch.empty(0, dtype=torch.uint16, device=cuda), key_bits=12, hist=h, accumulate=False)
+    assert int(h.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("nbins", [1, 2, 255, 256, 257, 4096, 65536, 65536 * 7 + 3])
+def test_exclusive_scan(cuda, nbins):
+    rng = np.random.default_rng(nbins)
+    C = rng.integers(0, 1 << 20, size=nbins, dtype=np.uint64)
+    if nbins > 3:
+        C[rng.integers(0, nbins, size=nbins // 3)] = 0
+    P = to_host(fs.exclusive_scan(to_dev(C.astype(np.int64), cuda))).astype(np.uint64)
+    np.testing.assert_array_equal(P, oracle.exclusive_scan(C))
+
+
+@pytest.mark.parametrize("dist", ["uniform", "const", "zipf"])
+def test_expand_ranges(cuda, dist):
+    keys = datagen.gen_u16(dist, 777_777, seed=4)
+    C = oracle.histogram_u16(keys)
+    P = oracle.exclusive_scan(C)
+    Pd = to_dev(P.astype(np.int64), cuda)
+    full = oracle.reconstruct_counts_u16(C)
+    n = keys.size
+    for (b, e) in [(0, n), (0, 1), (n - 1, n), (12345, 23456), (1, 9), (n // 3, 2 * n // 3), (5, 5)]:
+        out = to_host(fs.expand_u16(Pd, b, e))
+        np.testing.assert_array_equal(out, full[b:e])
+
+
+def test_expand_sparse_bins(cuda):
+    """Tiles spanning more bins than the staged slice (the L2 search fallback)."""
+    keys = np.concatenate([np.arange(0, 65536, 1, dtype=np.uint16),
+                           np.full(50_000, 7, dtype=np.uint16), np.array([65535] * 10, dtype=np.uint16)])
+    out = to_host(fs.sort_keys(to_dev(keys, cuda)))
+    np.testing.assert_array_equal(out, oracle.sort_u16(keys))
+
+
+# ------------------------------------------------------------------ full-size configs
+@pytest.mark.parametrize("cfg,dist,n", [
+    ("c1", "uniform", 1 << 20),
+    ("c2", "uniform", 1 << 28),
+    ("c3a", "zipf", 1 << 28),
+    ("c3b", "gauss", 1 << 28),
+    ("c3c", "sortedswap", 1 << 28),
+    ("c3d", "const", 1 << 28),
+])
+def test_full_size_configs(cuda, cfg, dist, n):
+    """BASELINE.json configs c1-c3 at full size, compared element by element."""
+    if dist in ("uniform", "zipf", "gauss", "const"):
+        t = torch.empty(n, dtype=torch.uint16, device=cuda)
+        datagen.gen_u16_device(t.data_ptr(), dist, n, seed=0, stream=torch.cuda.current_stream().cuda_stream)
+        keys = to_host(t)
+    else:
+        keys = datagen.gen_u16(dist, n, seed=0)
+        t = to_dev(keys, cuda)
+    out = to_host(fs.sort_keys(t))
+    want = oracle.sort_u16(keys)
+    np.testing.assert_array_equal(out, want)
+    if dist == "sortedswap":  # closed form: the sorted output is the pre-swap base array
+        base = ((np.arange(n, dtype=np.uint64) * 65536) // n).astype(np.uint16)
+        np.testing.assert_array_equal(out, base)
+
+
+def test_device_datagen_matches_host(cuda):
+    for dist in ["uniform", "zipf", "gauss", "const"]:
+        n = 1_000_003
+        t = torch.empty(n, dtype=torch.uint16, device=cuda)
+        datagen.gen_u16_device(t.data_ptr(), dist, n, seed=9, i0=12345, stream=torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(to_host(t), datagen.gen_u16(dist, n, seed=9, i0=12345, n_total=n + 12345))
+
+
+def test_host_streaming_sort(cuda):
+    n = (1 << 22) + 5
+    keys = datagen.gen_u16("gauss", n, seed=8)
+    src = torch.from_numpy(keys).pin_memory()
+    out = fs.sort_keys_u16_host(src, batch=1 << 20)
+    np.testing.assert_array_equal(out.numpy(), oracle.sort_u16(keys))
+    out2 = fs.sort_keys_u16_host(torch.from_numpy(keys), batch=0)  # pageable, default batch
+    np.testing.assert_array_equal(out2.numpy(), oracle.sort_u16(keys))
+
+
+def test_send_counts_matches_oracle(cuda):
+    rng = np.random.default_rng(0)
+    for G in [1, 2, 3, 8]:
+        hist_all = np.stack([oracle.histogram_u16(datagen.gen_u16("zipf", 10_000 + 37 * r, seed=r))
+                             for r in range(G)])
+        Hd = to_dev(hist_all.astype(np.int64), cuda)
+        for g in range(G):
+            got = to_host(fs.send_counts(Hd, g)).astype(np.uint64)
+            np.testing.assert_array_equal(got, oracle.send_counts(hist_all, g))
+    del rng
