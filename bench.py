@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="fs", choices=["fs", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default: config c2)")
+    ap.add_argument("--n", type=int, default=None, help="keys per GPU (default: the workload's size)")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3a", "c3b", "c3c", "c3d", "c5"],
+                    help="BASELINE.json config (c2 is the headline; the others are extra lines)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -179,6 +181,89 @@ def load_traffic(kernel: str):
     return None, None
 
 
+WORKLOADS = {
+    "c1": ("uniform", 1 << 20, "c1: 1,048,576 uint16 keys, uniform, seed 0 (L2-resident: launch-bound)"),
+    "c2": ("uniform", N_PER_GPU, WORKLOAD),
+    "c3a": ("zipf", N_PER_GPU, "c3a: 268,435,456 uint16 keys, Zipf s=1.2 with seeded value permutation, seed 0"),
+    "c3b": ("gauss", N_PER_GPU, "c3b: 268,435,456 uint16 keys, Gaussian(32768, 1024) rounded+clipped, seed 0"),
+    "c3c": ("sortedswap", N_PER_GPU, "c3c: 268,435,456 uint16 keys, sorted + floor(n/100) random pair swaps, seed 0"),
+    "c3d": ("const", N_PER_GPU, "c3d: 268,435,456 uint16 keys, all equal (0xA5A5)"),
+}
+
+
+def run_fs_pairs(args, dev):
+    """Config c5: 2^29 (u64 key uniform, u32 value = index) pairs, stable sort (one GPU)."""
+    import torch
+
+    import datagen
+    import paper_2605_10390_b200 as fs
+    from paper_2605_10390_b200 import _lib
+    L = fs.lib()
+    n = args.n or (1 << 29)
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+    k = torch.empty(n, dtype=torch.uint64, device=dev)
+    v = torch.empty(n, dtype=torch.uint32, device=dev)
+    datagen.gen_u64_device(k.data_ptr(), n, seed=0, stream=s)
+    datagen.iota_u32_device(v.data_ptr(), n, stream=s)
+    ko, vo = torch.empty_like(k), torch.empty_like(v)
+    temp = torch.empty(L.fs_sort_pairs_u64_u32_temp_bytes(n, 64), dtype=torch.uint8, device=dev)
+    nev = 2 + 8 + 1
+    steps = args.steps
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(steps)]
+    for row in events:
+        for e in row:
+            e.record(stream)
+    handles = [ctypes_array(row) for row in events]
+    torch.cuda.synchronize()
+
+    def step(h=None):
+        if h is not None:
+            L.fs_set_phase_events(h, nev)
+        _lib.check(L.fs_sort_pairs_u64_u32(k.data_ptr(), v.data_ptr(), ko.data_ptr(), vo.data_ptr(), n, 64,
+                                           temp.data_ptr(), temp.numel(), s), "fs_sort_pairs_u64_u32")
+        if h is not None:
+            L.fs_set_phase_events(None, 0)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        for i in range(steps):
+            step(handles[i])
+        torch.cuda.synchronize()
+    total_ms = events[0][0].elapsed_time(events[-1][nev - 1])
+    phase = [statistics.mean(r[i].elapsed_time(r[i + 1]) for r in events) for i in range(nev - 1)]
+    pass_ms = phase[1:9]
+    dom = max(range(8), key=lambda i: pass_ms[i])
+    peak, peak_src = measured_peak_gbs()
+    alg = 24 * n  # one pass reads and writes 8 B key + 4 B value per pair
+    achieved = alg / (pass_ms[dom] * 1e-3) / 1e9
+    t_step = total_ms / steps
+    line = {
+        "metric": METRIC, "value": round(n * steps / (total_ms * 1e-3) / 1e9, 3), "unit": "Gkeys/s", "n_gpus": 1,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "c5: 536,870,912 (u64 key uniform, u32 value = index) pairs, stable ascending sort",
+                   "pairs": n, "l2": "inputs (6 GiB) larger than L2: no flush"},
+        "roofline": {"bound": "hbm", "kernel": f"onesweep pass {dom}", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(pass_ms[dom], 4),
+                     "peak_source": peak_src},
+        "whole_step": {"minimal_bytes": 24 * n, "method_bytes_lsd8": 200 * n,
+                       "frac_minimal_of_measured_peak": round(24 * n / (t_step * 1e-3) / 1e9 / peak, 4),
+                       "method_GBps": round(200 * n / (t_step * 1e-3) / 1e9, 1)},
+        "phases_ms": {"digit_hist+plan": round(phase[0], 4), **{f"pass{i}": round(x, 4) for i, x in enumerate(pass_ms)},
+                      "identity_copy_check": round(phase[9], 4)},
+        "gpu_launches": (2 + 8 + 1) * steps,
+        "clocks": clocks.summary(),
+    }
+    if not args.no_verify:
+        import oracle
+        kin, kout, vout = k.cpu().numpy(), ko.cpu().numpy(), vo.cpu().numpy()
+        line["verified_invariants"] = oracle.check_pairs_index(kin, kout, vout) == 0
+    print(json.dumps(line), flush=True)
+
+
 def run_fs(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -189,15 +274,21 @@ def run_fs(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if args.workload == "c5":
+        return run_fs_pairs(args, dev)
     L = fs.lib()
-    n = args.n
+    dist_name, n_default, workload_text = WORKLOADS[args.workload]
+    n = args.n or n_default
     n_total = n * world
     i0 = rank * n
     stream = torch.cuda.current_stream(dev)
     s = stream.cuda_stream
 
     keys = torch.empty(n, dtype=torch.uint16, device=dev)
-    datagen.gen_u16_device(keys.data_ptr(), "uniform", n, seed=0, i0=i0, n_total=n_total, stream=s)
+    if dist_name == "sortedswap":
+        keys.copy_(torch.from_numpy(datagen.gen_u16("sortedswap", n_total, seed=0)[i0:i0 + n]))
+    else:
+        datagen.gen_u16_device(keys.data_ptr(), dist_name, n, seed=0, i0=i0, n_total=n_total, stream=s)
     out = torch.empty(n, dtype=torch.uint16, device=dev)
     dist = None
     if world > 1:
@@ -269,7 +360,7 @@ def run_fs(args, rank, world, local_rank):
     # Roofline of the dominant kernel (algorithmic bytes = 2 B/key read for the
     # histogram, 2 B/key written for the expansion).
     if world == 1:
-        names = {"hist16": phase_ms[0], "expand16": phase_ms[2]}
+        names = {"hist16": phase_ms[1], "expand16": phase_ms[2]}  # phase 0 is empty (no memset)
         scan_ms = phase_ms[1]
     else:
         names = {"hist16+merge": phase_ms[0], "expand16": phase_ms[3]}
@@ -285,10 +376,11 @@ def run_fs(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": WORKLOAD if n == N_PER_GPU else f"{n} uint16 keys per GPU, uniform, seed 0",
+        "config": {"workload": workload_text if n == n_default else f"{n} uint16 keys per GPU, {dist_name}, seed 0",
                    "keys_per_gpu": n, "keys_total": n_total, "parallelism": f"dp{world}",
                    "multi_gpu_mode": None if world == 1 else "B (histogram all-reduce + own-range expansion)",
-                   "l2": "inputs (512 MiB/GPU) larger than L2 (126 MB): no flush between steps"},
+                   "l2": ("inputs (512 MiB/GPU) larger than L2 (126 MB): no flush between steps" if n * 2 > 126e6
+                          else "L2-resident input (c1): launch-bound, no roofline claim")},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(dom_ms, 5),
@@ -297,21 +389,21 @@ def run_fs(args, rank, world, local_rank):
                        "frac_of_measured_peak": round(whole_bytes / (t_max / args.steps * 1e-3) / 1e9 / peak, 4),
                        "frac_of_8TBps": round(whole_bytes / (t_max / args.steps * 1e-3) / 8e12, 4)},
         "phases_ms": {k: round(v, 5) for k, v in zip(
-            (["hist16", "merge_scan", "expand16"] if world == 1 else ["hist16+merge", "nccl_allreduce", "scan", "expand16"]),
+            (["prologue", "hist16+merge+scan", "expand16"] if world == 1 else ["hist16+merge", "nccl_allreduce", "scan", "expand16"]),
             phase_ms)},
-        "gpu_launches": (3 if world == 1 else 4) * args.steps,
+        "gpu_launches": (2 if world == 1 else 3) * args.steps,
         "clocks": clocks.summary(),
     }
     del scan_ms
 
     # End to end through the public host-buffer API: H2D of the step's keys from
     # pinned memory, the sort, D2H of the sorted keys, every step.
-    if not args.no_e2e:
+    if not args.no_e2e and args.workload == "c2":
         line["e2e"] = e2e(args, L, _lib, keys, n, n_total, rank, world, dev, dist)
 
     if not args.no_verify and world == 1:
         line["verified"] = verify(out, keys)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         v, reps, dt, ok = time_oracle(n, 3, 0, min_seconds=10.0)
         line["cpu_baseline"] = {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
                                 "sample": f"the full c2 input (2^28 keys) sorted {reps} times ({dt:.1f} s) by the "

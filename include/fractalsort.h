@@ -188,8 +188,9 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
  * `count` cudaEvent_t handles (created by the caller), or NULL to disable.
  * While set, the sort calls made on THIS thread record events[i] on their
  * stream at phase boundaries, i < count:
- *   fs_sort_keys_u16:  [0] start, [1] after the histogram kernel, [2] after the
- *                      merge+scan kernel, [3] after the expansion kernel;
+ *   fs_sort_keys_u16:  [0] start, [1] after zeroing the temp counters, [2] after
+ *                      the histogram+merge+scan kernel, [3] after the expansion
+ *                      kernel;
  *   wide sorts:        [0] start, [1] after the digit histograms + plan,
  *                      [2 + p] after scatter pass p (passes ceil(key_bits/8)),
  *                      last after the identity copy check.

@@ -8,14 +8,15 @@
 // multi-GPU path writes only its own range (SURVEY.md §8(e) Mode B).
 //
 // B200 design: HBM-write bound (2 B per key).
-// Each CTA owns an output tile of kTile keys.  Warps 0 and 1 locate the first
-// and last bin touching the tile with a 32-ary search of P in L2 (4 rounds for
-// 65,536 bins); the tile's slice of P is staged in shared memory as 32-bit
-// offsets relative to the tile; each thread then emits 8 keys per 16-byte
-// streaming store (consecutive lanes -> consecutive 16 B), finding each run by
-// binary search in the staged slice (one search per vector unless a run
-// boundary falls inside it).  Unaligned head/tail keys are handled one per
-// thread by CTA 0.
+// Each CTA owns an output tile of 32,768 keys (64 KB).  The first and last bin
+// touching the tile are found by a block-parallel search of P (L2-resident):
+// one round over 256 coarse points, one round over the 256 points between them
+// (__syncthreads_count does the comparisons).  The tile's slice of P is staged
+// in shared memory as 32-bit offsets relative to the tile; each thread emits 8
+// keys per 16-byte streaming store (consecutive lanes -> consecutive 16 B) and
+// tracks its current run monotonically (its positions only increase).  The
+// kernel is launched with programmatic dependent launch so its launch overlaps
+// the histogram kernel's tail.  Unaligned head/tail keys: CTA 0, one per thread.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -23,30 +24,11 @@ namespace fs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kVecPerThread = 8;
-constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 16,384 keys = 32 KB
+constexpr int kVecPerThread = 16;
+constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 32,768 keys = 64 KB of output
 constexpr int kSliceCap = 4096;                                    // staged P entries
 
-// Largest v in [lo, hi) with P[v] <= o, given P[lo] <= o.  Whole warp participates.
-FS_DEVINL uint64_t warp_last_le(const uint64_t* __restrict__ P, uint64_t lo, uint64_t hi, uint64_t o) {
-  const uint32_t lane = lane_id();
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + lane * step;
-    const bool ok = idx < hi && __ldcg(P + idx) <= o;
-    const uint32_t m = __ballot_sync(kFull, ok);  // lane 0 always set
-    const uint32_t L = 31 - __clz(m);
-    lo = lo + L * step;
-    const uint64_t nhi = lo + step;
-    hi = nhi < hi ? nhi : hi;
-  }
-  const uint64_t idx = lo + lane;
-  const bool ok = idx < hi && __ldcg(P + idx) <= o;
-  const uint32_t m = __ballot_sync(kFull, ok);
-  return lo + (31 - __clz(m));
-}
-
-// Thread-level binary search over global P: largest v in [lo, hi) with P[v] <= o.
+// Thread-level binary search over global P: largest v in [lo, hi) with P[v] <= o, given P[lo] <= o.
 FS_DEVINL uint64_t thread_last_le(const uint64_t* __restrict__ P, uint64_t lo, uint64_t hi, uint64_t o) {
   while (hi - lo > 1) {
     const uint64_t mid = lo + (hi - lo) / 2;
@@ -55,8 +37,15 @@ FS_DEVINL uint64_t thread_last_le(const uint64_t* __restrict__ P, uint64_t lo, u
   return lo;
 }
 
-// Largest j in [lo, hi) with rel[j] <= l, given rel[lo] <= l.
-FS_DEVINL uint32_t smem_last_le(const uint32_t* rel, uint32_t lo, uint32_t hi, uint32_t l) {
+// Largest j in [j0, hi) with rel[j] <= l, given rel[j0] <= l: a short linear
+// probe (runs are usually long) then binary search.
+FS_DEVINL uint32_t advance(const uint32_t* rel, uint32_t j, uint32_t hi, uint32_t l) {
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (j + 1 >= hi || rel[j + 1] > l) return j;
+    ++j;
+  }
+  uint32_t lo = j;
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
     if (rel[mid] <= l) lo = mid; else hi = mid;
@@ -64,62 +53,72 @@ FS_DEVINL uint32_t smem_last_le(const uint32_t* rel, uint32_t lo, uint32_t hi, u
   return lo;
 }
 
-struct ExpandSmem {
-  uint64_t v_lo, v_hi;
-  uint32_t rel[kSliceCap];
-};
+// Block-wide: largest v < nbins with P[v] <= o for two positions at once, in two
+// rounds of loads (256-way coarse, then fine).  All threads get the results.
+FS_DEVINL void block_last_le2(const uint64_t* __restrict__ P, uint64_t nbins, uint64_t o_a, uint64_t o_b,
+                              uint64_t& v_a, uint64_t& v_b) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t cs = (nbins + kThreads - 1) / kThreads;  // coarse stride (<= 256 for nbins <= 65536)
+  const uint64_t ci = (uint64_t)tid * cs;
+  uint64_t p = ci < nbins ? __ldcg(P + ci) : ~0ull;
+  const uint64_t c_a = (uint64_t)__syncthreads_count(p <= o_a) - 1;  // P[0] = 0 <= o
+  const uint64_t c_b = (uint64_t)__syncthreads_count(p <= o_b) - 1;
+  const uint64_t fa = c_a * cs + tid, fb = c_b * cs + tid;
+  const bool in_a = tid < cs && fa < nbins, in_b = tid < cs && fb < nbins;
+  const uint64_t pa = in_a ? __ldcg(P + fa) : ~0ull;
+  const uint64_t pb = in_b ? __ldcg(P + fb) : ~0ull;
+  v_a = c_a * cs + (uint64_t)__syncthreads_count(pa <= o_a) - 1;
+  v_b = c_b * cs + (uint64_t)__syncthreads_count(pb <= o_b) - 1;
+}
 
 __global__ void __launch_bounds__(kThreads)
     k_expand16(const uint64_t* __restrict__ P, uint64_t nbins, uint64_t pos0, uint64_t nvec,
                uint16_t* __restrict__ out_body, uint64_t out_begin, uint64_t head, uint64_t tail_pos,
                uint64_t tail_n, uint16_t* __restrict__ out) {
-  __shared__ ExpandSmem sm;
-  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  __shared__ uint32_t rel[kSliceCap];
+  const uint32_t tid = threadIdx.x;
+  // Programmatic dependent launch: everything above overlaps the producer's tail;
+  // P is read only after the producer grid has completed.
+  cudaGridDependencySynchronize();
 
   // Unaligned head/tail keys (< 8 each): one per thread in CTA 0.
   if (blockIdx.x == 0 && tid < head + tail_n) {
     const uint64_t j = tid < head ? out_begin + tid : tail_pos + (tid - head);
-    const uint64_t v = thread_last_le(P, 0, nbins, j);
-    out[j - out_begin] = (uint16_t)v;
+    out[j - out_begin] = (uint16_t)thread_last_le(P, 0, nbins, j);
   }
   if (nvec == 0) return;
 
   const uint64_t vec0 = (uint64_t)blockIdx.x * (kTile / 8);
   const uint64_t vec_end = vec0 + kTile / 8 < nvec ? vec0 + kTile / 8 : nvec;
-  const uint64_t o0 = pos0 + vec0 * 8;                 // first global position of the tile
+  const uint64_t o0 = pos0 + vec0 * 8;  // first global position of the tile
   const uint32_t len = (uint32_t)((vec_end - vec0) * 8);
-  if (warp == 0) {
-    const uint64_t v = warp_last_le(P, 0, nbins, o0);
-    if (lane_id() == 0) sm.v_lo = v;
-  } else if (warp == 1) {
-    const uint64_t v = warp_last_le(P, 0, nbins, o0 + len - 1);
-    if (lane_id() == 0) sm.v_hi = v;
-  }
-  __syncthreads();
-  const uint64_t v_lo = sm.v_lo, v_hi = sm.v_hi;
+  uint64_t v_lo, v_hi;
+  block_last_le2(P, nbins, o0, o0 + len - 1, v_lo, v_hi);
   const uint64_t m = v_hi - v_lo + 2;  // P[v_lo .. v_hi+1]
   uint4* dst = reinterpret_cast<uint4*>(out_body) + vec0;
 
   if (m <= (uint64_t)kSliceCap) {
     for (uint32_t j = tid; j < m; j += kThreads) {
       const uint64_t p = __ldcg(P + v_lo + j);
-      sm.rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
+      rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
     }
     __syncthreads();
-    const uint32_t mm = (uint32_t)m;
-#pragma unroll
+    const uint32_t hi = (uint32_t)m - 1;  // searches stay below the sentinel rel[m-1] >= len
+    uint32_t j = 0;                       // rel[0] = 0: valid start for every position
+#pragma unroll 4
     for (int k = 0; k < kVecPerThread; ++k) {
       const uint32_t q = k * kThreads + tid;
       const uint32_t l = q * 8;
       if (l >= len) break;
-      uint32_t j = smem_last_le(sm.rel, 0, mm - 1, l);
-      uint32_t run_end = sm.rel[j + 1];
+      j = advance(rel, j, hi, l);
+      uint32_t run_end = rel[j + 1];
       uint32_t packed[4];
-      if (l + 7 < run_end) {  // whole vector inside one run (common case)
+      if (l + 7 < run_end) {  // the whole vector lies in one run (common case)
         const uint32_t v = (uint32_t)(v_lo + j);
         const uint32_t pv = v | (v << 16);
         packed[0] = packed[1] = packed[2] = packed[3] = pv;
       } else {
+        uint32_t jj = j;
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
           uint32_t pair = 0;
@@ -127,10 +126,10 @@ __global__ void __launch_bounds__(kThreads)
           for (int h = 0; h < 2; ++h) {
             const uint32_t pos = l + e + h;
             if (pos >= run_end) {
-              j = smem_last_le(sm.rel, j + 1, mm - 1, pos);
-              run_end = sm.rel[j + 1];
+              jj = advance(rel, jj, hi, pos);
+              run_end = rel[jj + 1];
             }
-            pair |= ((uint32_t)(v_lo + j) & 0xFFFFu) << (16 * h);
+            pair |= ((uint32_t)(v_lo + jj) & 0xFFFFu) << (16 * h);
           }
           packed[e / 2] = pair;
         }
@@ -175,9 +174,19 @@ cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out
   const uint64_t tail_pos = pos0 + nvec * 8;
   uint64_t grid = (nvec * 8 + kTile - 1) / kTile;
   if (grid == 0) grid = 1;
-  k_expand16<<<(unsigned)grid, kThreads, 0, s>>>(prefix, nbins, pos0, nvec, out + head, out_begin, head, tail_pos,
-                                                 tail_n, out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  uint16_t* body = out + head;
+  return cudaLaunchKernelEx(&cfg, k_expand16, prefix, nbins, pos0, nvec, body, out_begin, head, tail_pos, tail_n,
+                            out);
 }
 
 }  // namespace fs

@@ -1,45 +1,60 @@
-// hist16.cu — stage 1 of the u16 path: the per-SM compressed histogram (G1).
+// hist16.cu — stages 1 and 2 of the u16 path (G1 + G2): the per-SM compressed
+// histogram, the merge of the per-SM histograms, and the exclusive scan, in one
+// cooperative kernel.
 //
 // What it computes (§III.B.1 Fractal RMW, Alg. 1):
 // every key increments the counter of the leaf its MSB-first bit path selects;
 // at p = 16 the leaf slot is the key itself (ledger 1; computable pointers,
 // PAPER.md:196-215).  The trie's internal levels are sums of leaves (SIBLING
 // SUM), so only the leaf level is materialised; the scan builds
-// the rest implicitly.
+// the rest implicitly.  Then C[v] = sum over SMs (the two-step
+// local -> global merge) and P[v] = sum_{u<v} C[u] =
+// GetIndex(v) for every v (Alg. 3).
 //
 // B200 design:
-//  * One CTA of 1024 threads per SM; the 65,536-bin local tree lives in shared
-//    memory as 16-bit counters packed two per 32-bit word (128 KB): counter-width
-//    tapering (§III.D.1) is what makes a privatised 65,536-bin
-//    histogram fit in one SM (n_L = W/w_c = 2 counters per word).
-//    Bin v lives in word v>>1, half v&1, so the packed partial is exactly a u16
-//    array indexed by bin.
-//  * Keys stream in as 128-bit loads (8 keys) with evict-first, one vector
-//    look-ahead per unrolled group to keep bytes in flight.
+//  * Cooperative launch, one CTA of 1024 threads per SM.  The 65,536-bin local
+//    tree lives in shared memory as 16-bit counters packed two per 32-bit word
+//    (128 KB): counter-width tapering (§III.D.1) is what makes a
+//    privatised 65,536-bin histogram fit in one SM (n_L = W/w_c = 2 counters
+//    per word).  Bin v lives in word v>>1, half v&1, so a packed
+//    partial is exactly a u16 array indexed by bin.
+//  * Keys stream in as 128-bit evict-first loads, two vectors (16 keys) per
+//    thread per group.  The loop is bound by the shared-memory atomic unit
+//    (~3.5 wavefronts per warp-wide random atomic from bank conflicts); the
+//    micro-benchmarks behind these choices are in DESIGN.md §Kernels/hist16.
 //  * Overflow ("Counter Width Compression and Overflow", ledger 12):
-//    never wraps.  Every shared atomic returns the old word; a thread that sees
-//    either half >= THETA (2^14) atomically exchanges the word with 0 and adds
-//    both halves to the global u64 spill array.  Between the increment that
-//    lifts a counter to >= THETA and the first exchange, each thread can add at
-//    most the keys of one unrolled group (UNROLL*8) to it, because it checks the
-//    returned values before its next group; so a counter never exceeds
-//    THETA + 255 + 1024*UNROLL*8 = 49,407 < 65,536 (UNROLL = 4).  No barrier.
-//  * Runs of equal keys (sorted or constant inputs, ledger 21-22) are aggregated:
-//    a thread whose 8 keys are equal issues one +8; a warp whose 256 keys are
-//    all equal issues one +256 from lane 0 (same-address atomics serialise).
-//  * At the end the CTA writes its 128 KB partial to partials[blockIdx.x]
-//    (L2-resident) for the merge in scan.cu (PAPER.md:89 two-step merge).
+//    never wraps.  Every shared atomic returns the old word; the returns of a
+//    group are OR-ed and tested once.  If either half of any returned word was
+//    >= THETA = 2^15, the thread re-reads each word it touched and atomically
+//    exchanges every word that is still hot with 0, adding both halves to the
+//    global u64 spill array.  Between the increment that lifts a counter to
+//    >= THETA and the first exchange, each thread adds at most one group (16
+//    keys) to it, because it tests before its next group; so a counter never
+//    exceeds THETA + 255 + 1024 * 16 = 49,407 < 65,536.  No barrier is needed.
+//  * Runs of equal keys (sorted or constant inputs, ledger 21-22): a warp that
+//    sees an all-equal vector switches to an aggregating mode (one +8 per
+//    thread or one +256 per warp instead of same-address atomics); the check is
+//    sampled every 4th group while not aggregating.
+//  * Prologue zeroes the spill array and slice flags (grid-strided) and the
+//    grid synchronises once, so the call needs no memset node.
+//  * Tail: each CTA flushes its partial (L2-resident), grid sync, then 128
+//    slices of 512 bins are merged (16 row groups x 64 columns of 16-byte
+//    loads), and each slice's exclusive base is the sum of all earlier slice
+//    totals read in parallel (one round of loads, no serial lookback chain).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fs {
 namespace {
 
 constexpr int kThreads = 1024;
-constexpr int kUnroll = 4;              // 128-bit vectors per thread per group
-constexpr uint32_t kHotMask = 0xC000C000u;  // either 16-bit half >= 2^14
-
-static_assert(16384 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violated");
+constexpr int kUnroll = 2;                  // 128-bit vectors per thread per group
+constexpr uint32_t kHotMask = 0x80008000u;  // either 16-bit half >= 2^15
+static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violated");
 
 FS_DEVINL void spill_word(uint32_t* sh, uint32_t w, unsigned long long* spill) {
   const uint32_t x = atomicExch(&sh[w], 0u);
@@ -54,20 +69,30 @@ FS_DEVINL void add_key(uint32_t* sh, uint32_t k, uint32_t cnt, unsigned long lon
   if (old & kHotMask) spill_word(sh, w, spill);
 }
 
-// Plain path: 8 independent atomics, returns checked after all are issued.
-FS_DEVINL void add8(uint32_t* sh, const uint4& v, unsigned long long* spill) {
+// 8 atomics; returns the OR of the old words.  Word byte offset of the low key
+// of x is (x & 0xFFFE) * 2, of the high key (x >> 17) * 4; the increment is 1 or
+// 0x10000 by the key's lowest bit.
+FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  uint32_t old[8];
+  char* base = reinterpret_cast<char*>(sh);
+  uint32_t acc = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;
-    old[2 * j] = atomicAdd(&sh[lo >> 1], (lo & 1u) ? 0x10000u : 1u);
-    old[2 * j + 1] = atomicAdd(&sh[hi >> 1], (hi & 1u) ? 0x10000u : 1u);
+    const uint32_t x = w[j];
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
   }
+  return acc;
+}
+
+// Slow path after a hot return: exchange every touched word that is still hot.
+FS_DEVINL void recheck8(uint32_t* sh, const uint4& v, unsigned long long* spill) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    if (old[2 * j] & kHotMask) spill_word(sh, (w[j] & 0xFFFFu) >> 1, spill);
-    if (old[2 * j + 1] & kHotMask) spill_word(sh, w[j] >> 17, spill);
+    const uint32_t a = (w[j] & 0xFFFFu) >> 1, b = w[j] >> 17;
+    if (sh[a] & kHotMask) spill_word(sh, a, spill);
+    if (sh[b] & kHotMask) spill_word(sh, b, spill);
   }
 }
 
@@ -85,62 +110,178 @@ FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill)
     if (lane_id() == 0) add_key(sh, k0, 256u, spill);
   } else if (eq) {
     add_key(sh, k0, 8u, spill);
-  } else {
-    add8(sh, v, spill);
+  } else if (add8(sh, v) & kHotMask) {
+    recheck8(sh, v, spill);
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    k_hist16(const uint16_t* __restrict__ keys, uint64_t n, uint64_t head, uint64_t nvec,
-             uint32_t* __restrict__ partials, unsigned long long* __restrict__ spill) {
+constexpr int kSliceBins = 512;                    // merge/scan granularity
+constexpr int kSlices = kHistBins / kSliceBins;    // 128
+constexpr int kSliceVec = kSliceBins / 8;          // uint4 per partial row per slice (64)
+constexpr int kRowGroups = kThreads / kSliceVec;   // 16
+static_assert(kSlices == kHistSlices, "slice count");
+
+struct HistArgs {
+  const uint16_t* keys;
+  uint64_t n, head, nvec;
+  uint32_t* partials;                  // grid x kHistWords packed u16 pairs
+  unsigned long long* spill;           // 65536 u64 (zeroed in the prologue)
+  uint64_t* hist_out;                  // optional: C written (+=) for v < nbins_out
+  uint64_t nbins_out;
+  int accumulate;
+  uint64_t* prefix;                    // optional: 65537 exclusive prefix (the sort path)
+  unsigned long long* slice_status;    // kSlices words (zeroed in the prologue)
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   extern __shared__ uint4 smem_v4[];
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem_v4);
+  const uint32_t tid = threadIdx.x;
+  cg::grid_group grid = cg::this_grid();
 
-  // zero the local tree (128 KB)
+  // ---------------- prologue: zero the local tree, the spill array and the flags
 #pragma unroll
-  for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[threadIdx.x + i * kThreads] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
+  for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins; i += gridDim.x * kThreads) a.spill[i] = 0;
+  if (blockIdx.x == 0 && tid < kSlices) a.slice_status[tid] = 0;
+  grid.sync();
 
+  // ---------------- stage 1: local compressed histogram
   // Unaligned head and ragged tail (< 8 + 7 keys) go to the last CTA, one key per thread.
   if (blockIdx.x == gridDim.x - 1) {
-    const uint64_t tail0 = head + nvec * 8;
-    const uint64_t nscalar = head + (n - tail0);
-    for (uint64_t t = threadIdx.x; t < nscalar; t += kThreads) {
-      const uint64_t idx = t < head ? t : tail0 + (t - head);
-      add_key(sh, keys[idx], 1u, spill);
+    const uint64_t tail0 = a.head + a.nvec * 8;
+    const uint64_t nscalar = a.head + (a.n - tail0);
+    for (uint64_t t = tid; t < nscalar; t += kThreads) {
+      const uint64_t idx = t < a.head ? t : tail0 + (t - a.head);
+      add_key(sh, a.keys[idx], 1u, a.spill);
     }
   }
-
-  const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(keys + head);
+  const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(a.keys + a.head);
+  const uint64_t nvec = a.nvec;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-
-  // Main loop: groups of kUnroll vectors at grid stride.  The bound is tested on
-  // the warp's last lane so the whole warp iterates together (warp collectives).
+  uint64_t i = (uint64_t)blockIdx.x * kThreads + tid;
+  // The bound is tested on the warp's last lane so the whole warp iterates
+  // together (warp collectives inside).
   const uint64_t warp_tail = 31 - lane_id();
+  bool agg = false;
+  uint32_t phase = 0;
   for (; i + warp_tail + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
     uint4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream_v4(vec + i + u * stride);
-    bool runs = false;
+    if (agg || phase == 0) {
+      bool runs = false;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) runs |= all8_equal(v[u]);
-    if (__any_sync(kFull, runs)) {
+      for (int u = 0; u < kUnroll; ++u) runs |= all8_equal(v[u]);
+      agg = __any_sync(kFull, runs);
+    }
+    phase = (phase + 1) & 3;
+    if (agg) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], spill);
+      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill);
     } else {
+      uint32_t acc = 0;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add8(sh, v[u], spill);
+      for (int u = 0; u < kUnroll; ++u) acc |= add8(sh, v[u]);
+      if (acc & kHotMask) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) recheck8(sh, v[u], a.spill);
+      }
     }
   }
-  // Remainder vectors (fewer than kUnroll per thread).
-  for (; i < nvec; i += stride) add8(sh, ld_stream_v4(vec + i), spill);
-
+  for (; i < nvec; i += stride) {
+    const uint4 q = ld_stream_v4(vec + i);
+    if (add8(sh, q) & kHotMask) recheck8(sh, q, a.spill);
+  }
   __syncthreads();
+
   // Flush the local tree: the first step of the two-step merge.
-  uint4* dst = reinterpret_cast<uint4*>(partials + (uint64_t)blockIdx.x * kHistWords);
+  uint4* dst = reinterpret_cast<uint4*>(a.partials + (uint64_t)blockIdx.x * kHistWords);
 #pragma unroll
-  for (int j = 0; j < kHistWords / 4 / kThreads; ++j) dst[threadIdx.x + j * kThreads] = smem_v4[threadIdx.x + j * kThreads];
+  for (int j = 0; j < kHistWords / 4 / kThreads; ++j) dst[tid + j * kThreads] = smem_v4[tid + j * kThreads];
+  grid.sync();
+  // The dependent kernel (expansion) may start launching; it waits for this
+  // grid's completion before reading P (programmatic dependent launch).
+  cudaTriggerProgrammaticLaunchCompletion();
+
+  // ---------------- stage 1b: merge, one 512-bin slice at a time
+  const int G = gridDim.x;
+  uint32_t* part = sh;                                                                       // [16][512] u32
+  unsigned long long* wsum = reinterpret_cast<unsigned long long*>(sh + kRowGroups * kSliceBins);  // [16]
+  const uint32_t col = tid % kSliceVec, rg = tid / kSliceVec;
+  for (int slice = blockIdx.x; slice < kSlices; slice += G) {
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint4* src = reinterpret_cast<const uint4*>(a.partials) + (uint64_t)slice * kSliceVec + col;
+    int g = rg;
+    for (; g + 3 * kRowGroups < G; g += 4 * kRowGroups) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldcg(src + (uint64_t)(g + u * kRowGroups) * (kHistWords / 4));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[0] += q[u].x & 0xFFFFu; acc[1] += q[u].x >> 16; acc[2] += q[u].y & 0xFFFFu; acc[3] += q[u].y >> 16;
+        acc[4] += q[u].z & 0xFFFFu; acc[5] += q[u].z >> 16; acc[6] += q[u].w & 0xFFFFu; acc[7] += q[u].w >> 16;
+      }
+    }
+    for (; g < G; g += kRowGroups) {
+      const uint4 q = __ldcg(src + (uint64_t)g * (kHistWords / 4));
+      acc[0] += q.x & 0xFFFFu; acc[1] += q.x >> 16; acc[2] += q.y & 0xFFFFu; acc[3] += q.y >> 16;
+      acc[4] += q.z & 0xFFFFu; acc[5] += q.z >> 16; acc[6] += q.w & 0xFFFFu; acc[7] += q.w >> 16;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[rg * kSliceBins + col * 8 + j] = acc[j];
+    __syncthreads();
+    unsigned long long c = 0;
+    const uint32_t bin = slice * kSliceBins + tid;
+    if (tid < kSliceBins) {
+#pragma unroll
+      for (int r = 0; r < kRowGroups; ++r) c += part[r * kSliceBins + tid];
+      c += a.spill[bin];
+      if (a.hist_out && bin < a.nbins_out) a.hist_out[bin] = a.accumulate ? a.hist_out[bin] + c : c;
+    }
+    if (a.prefix) {
+      // slice-local exclusive scan; the slice's base is added in stage 2
+      const unsigned long long inc = warp_inclusive_scan<unsigned long long>(c);
+      if ((tid & 31) == 31 && tid < kSliceBins) wsum[tid >> 5] = inc;
+      __syncthreads();
+      unsigned long long off = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kSliceBins / 32; ++w) {
+        const unsigned long long t = wsum[w];
+        if (w < (int)(tid >> 5)) off += t;
+        tot += t;
+      }
+      if (tid < kSliceBins) a.prefix[bin] = off + inc - c;
+      if (tid == 0) st_release_u64(&a.slice_status[slice], kFlagAggregate | tot);
+    }
+    __syncthreads();
+  }
+  if (!a.prefix) return;
+
+  // ---------------- stage 2: exclusive scan across slices (GetIndex, Alg. 3)
+  // Each slice's base is the sum of all earlier slice totals, read in parallel
+  // (128 slices: one round of loads instead of a serial lookback chain).
+  __shared__ unsigned long long base_sh[kThreads / 32];
+  for (int slice = blockIdx.x; slice < kSlices; slice += G) {
+    unsigned long long t = 0;
+    if ((int)tid < slice) {
+      unsigned long long s;
+      do { s = ld_acquire_u64(&a.slice_status[tid]); } while ((s >> 62) == 0);
+      t = s & kValueMask;
+    }
+    t = warp_sum(t);
+    if ((tid & 31) == 0) base_sh[tid >> 5] = t;
+    __syncthreads();
+    unsigned long long base = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) base += base_sh[w];
+    const uint32_t bin = slice * kSliceBins + tid;
+    if (tid < kSliceBins) {
+      a.prefix[bin] += base;
+      if (bin == kHistBins - 1) a.prefix[kHistBins] = base + (ld_acquire_u64(&a.slice_status[slice]) & kValueMask);
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -152,19 +293,32 @@ int hist16_grid(uint64_t n) {
   return g ? (int)g : 1;
 }
 
-cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill, int grid,
-                          cudaStream_t s) {
+cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill,
+                          uint64_t* hist_out, uint64_t nbins_out, int accumulate, uint64_t* prefix,
+                          unsigned long long* slice_status, int grid, cudaStream_t s) {
   static_assert(kHistWords % (4 * kThreads) == 0, "flush mapping");
+  static_assert(kRowGroups * kSliceBins * 4 + 16 * 8 <= kHistWords * 4, "merge smem");
   constexpr int smem = kHistWords * 4;
   cudaError_t e = cudaFuncSetAttribute(k_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  HistArgs a;
+  a.keys = keys;
+  a.n = n;
   // 16-byte aligned body: head keys before it, nvec full vectors, then the tail.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
-  uint64_t head = ((16 - (addr & 15)) & 15) / 2;
-  if (head > n) head = n;
-  const uint64_t nvec = (n - head) / 8;
-  k_hist16<<<grid, kThreads, smem, s>>>(keys, n, head, nvec, partials, spill);
-  return cudaGetLastError();
+  a.head = ((16 - (addr & 15)) & 15) / 2;
+  if (a.head > n) a.head = n;
+  a.nvec = (n - a.head) / 8;
+  a.partials = partials;
+  a.spill = spill;
+  a.hist_out = hist_out;
+  a.nbins_out = nbins_out;
+  a.accumulate = accumulate;
+  a.prefix = prefix;
+  a.slice_status = slice_status;
+  void* args[] = {&a};
+  // Cooperative launch: all CTAs co-resident (one per SM), so grid.sync() is safe.
+  return cudaLaunchCooperativeKernel((const void*)k_hist16, dim3(grid), dim3(kThreads), args, smem, s);
 }
 
 }  // namespace fs

@@ -10,13 +10,11 @@ namespace fs {
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-// Temp layout of the u16 path (all offsets 256-byte aligned).  The first
-// zero_bytes (spill counters, scan status words, scan ticket) are zeroed by one
-// cudaMemsetAsync per call.
+// Temp layout of the u16 path (all offsets 256-byte aligned).  Nothing needs
+// zeroing by the caller: the histogram kernel zeroes its spill and flags.
 struct U16Layout {
   int grid = 1;
-  size_t spill_off = 0, status_off = 0, ticket_off = 0, zero_bytes = 0;
-  size_t partials_off = 0, prefix_off = 0, total = 0;
+  size_t spill_off = 0, slice_status_off = 0, partials_off = 0, prefix_off = 0, total = 0;
 };
 U16Layout u16_layout(uint64_t n, bool with_prefix);
 

@@ -19,10 +19,15 @@ const DeviceInfo& device_info();
 // Per-SM compressed histogram of u16 keys (stage 1).  One CTA per SM.
 constexpr int kHistBins = 65536;
 constexpr int kHistWords = kHistBins / 2;  // two 16-bit counters per 32-bit word
+constexpr int kHistSlices = 128;            // 512-bin merge/scan slices
 int hist16_grid(uint64_t n);
-// partials: grid x kHistWords packed words; spill: 65536 u64, must be zero on entry.
+// Cooperative launch, one CTA per SM: local histograms -> partials, grid sync,
+// merge (C written to hist_out if non-null, += when accumulate), and, when
+// prefix != nullptr, the exclusive scan P[0..65536].  spill (65536 u64) and
+// slice_status (kHistSlices u64) are scratch; the kernel zeroes them itself.
 cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill,
-                          int grid, cudaStream_t s);
+                          uint64_t* hist_out, uint64_t nbins_out, int accumulate, uint64_t* prefix,
+                          unsigned long long* slice_status, int grid, cudaStream_t s);
 
 // ---------------------------------------------------------------- scan.cu
 constexpr int kScanTileBins = 256;

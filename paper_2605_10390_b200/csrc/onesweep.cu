@@ -163,7 +163,14 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = 0; i < kItems; ++i) {
     const bool valid = chunk0 + 32 * i + lane < n;
     const uint32_t d = digit_of(key[i], shift);
-    const uint32_t peers = __match_any_sync(kFull, valid ? d : (0x100u | lane));
+    // lanes holding the same digit: 8 ballots (match.any is far slower on sm_100a)
+    uint32_t peers = __ballot_sync(kFull, valid);
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t vote = __ballot_sync(kFull, bit);
+      peers &= bit ? vote : ~vote;
+    }
     const uint32_t leader = 31 - __clz(peers);
     uint32_t old = 0;
     if (valid && lane == leader) {
