@@ -22,7 +22,11 @@ FS_DEVINL void st_stream_v4(uint4* p, uint4 v) {
                : "memory");
 }
 
-// GPU-scope release store / acquire load of a 64-bit status word (decoupled lookback).
+// 64-bit status words of the decoupled lookbacks.  A status word carries its own
+// value (flag | count), and nothing else is published through it, so relaxed
+// GPU-scope accesses suffice.  (On sm_100a ld.acquire.gpu compiles to
+// LDG.STRONG + CCTL.IVALL -- an L1 invalidate per poll -- and st.release to a
+// MEMBAR; both were the top stalls of the first onesweep.)
 FS_DEVINL void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

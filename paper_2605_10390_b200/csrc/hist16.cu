@@ -100,15 +100,21 @@ FS_DEVINL bool all8_equal(const uint4& v) {
   return (v.x == v.y) & (v.y == v.z) & (v.z == v.w) & ((v.x >> 16) == (v.x & 0xFFFFu));
 }
 
-// Aggregating path for a vector when the warp has runs of equal keys.
+// Aggregating path for a vector when the warp has runs of equal keys.  Lanes
+// whose 8 keys all equal lane 0's key (or lane 31's: a run boundary inside the
+// warp) are counted by one atomic of 8 * (number of such lanes) <= 256; other
+// all-equal lanes add 8; the rest take the plain path.
 FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill) {
+  const uint32_t lane = lane_id();
   const bool eq = all8_equal(v);
   const uint32_t k0 = v.x & 0xFFFFu;
-  const uint32_t lane0_key = __shfl_sync(kFull, k0, 0);  // every lane must execute the shuffle
-  const bool warp_same = __all_sync(kFull, eq && k0 == lane0_key);
-  if (warp_same) {
-    if (lane_id() == 0) add_key(sh, k0, 256u, spill);
-  } else if (eq) {
+  const uint32_t ka = __shfl_sync(kFull, k0, 0), kb = __shfl_sync(kFull, k0, 31);  // all lanes shuffle
+  const uint32_t ma = __ballot_sync(kFull, eq && k0 == ka);
+  const uint32_t mb = __ballot_sync(kFull, eq && k0 == kb && k0 != ka);
+  if (lane == 0 && ma) add_key(sh, ka, 8u * __popc(ma), spill);
+  if (lane == 31 && mb) add_key(sh, kb, 8u * __popc(mb), spill);
+  if (((ma | mb) >> lane) & 1u) return;
+  if (eq) {
     add_key(sh, k0, 8u, spill);
   } else if (add8(sh, v) & kHotMask) {
     recheck8(sh, v, spill);
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
         tot += t;
       }
       if (tid < kSliceBins) a.prefix[bin] = off + inc - c;
-      if (tid == 0) st_release_u64(&a.slice_status[slice], kFlagAggregate | tot);
+      if (tid == 0) st_relaxed_u64(&a.slice_status[slice], kFlagAggregate | tot);
     }
     __syncthreads();
   }
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     unsigned long long t = 0;
     if ((int)tid < slice) {
       unsigned long long s;
-      do { s = ld_acquire_u64(&a.slice_status[tid]); } while ((s >> 62) == 0);
+      do { s = ld_relaxed_u64(&a.slice_status[tid]); } while ((s >> 62) == 0);
       t = s & kValueMask;
     }
     t = warp_sum(t);
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     const uint32_t bin = slice * kSliceBins + tid;
     if (tid < kSliceBins) {
       a.prefix[bin] += base;
-      if (bin == kHistBins - 1) a.prefix[kHistBins] = base + (ld_acquire_u64(&a.slice_status[slice]) & kValueMask);
+      if (bin == kHistBins - 1) a.prefix[kHistBins] = base + (ld_relaxed_u64(&a.slice_status[slice]) & kValueMask);
     }
     __syncthreads();
   }

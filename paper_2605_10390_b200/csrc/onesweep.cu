@@ -33,8 +33,8 @@ constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTileKeys = kThreads * kItems;  // 4096
+constexpr int kItems = 12;
+constexpr int kTileKeys = kThreads * kItems;  // 3072
 static_assert(kThreads == kRadix, "one thread per digit in the lookback");
 
 constexpr unsigned long long kStFlagAgg = 1ull << 62;
@@ -115,7 +115,7 @@ struct PassSmem {
 };
 
 template <typename K, bool kHasValues>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     k_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kX,
                uint32_t* __restrict__ vX, K* __restrict__ kY, uint32_t* __restrict__ vY, uint64_t n, int pass,
                const Plan* __restrict__ plan, unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket) {
@@ -199,18 +199,18 @@ __global__ void __launch_bounds__(kThreads)
   unsigned long long* st = status + tile * kRadix + d;
   unsigned long long excl = 0;
   if (tile == 0) {
-    st_release_u64(st, kStFlagInc | tag | cnt);
+    st_relaxed_u64(st, kStFlagInc | tag | cnt);
   } else {
-    st_release_u64(st, kStFlagAgg | tag | cnt);
+    st_relaxed_u64(st, kStFlagAgg | tag | cnt);
     int64_t t = (int64_t)tile - 1;
     while (true) {
-      const unsigned long long s = ld_acquire_u64(status + (uint64_t)t * kRadix + d);
+      const unsigned long long s = ld_relaxed_u64(status + (uint64_t)t * kRadix + d);
       if ((s & (0x3Full << kTagShift)) != tag || (s >> 62) == 0) continue;  // not yet published
       excl += s & kStValue;
       if ((s >> 62) == 2 || t == 0) break;
       --t;
     }
-    st_release_u64(st, kStFlagInc | tag | (excl + cnt));
+    st_relaxed_u64(st, kStFlagInc | tag | (excl + cnt));
   }
   __syncthreads();
   uint32_t woff = 0;

@@ -103,15 +103,15 @@ __global__ void __launch_bounds__(kThreads)
   if (warp == 0) {
     unsigned long long excl = 0;
     if (tile == 0) {
-      if (lane == 0) st_release_u64(&status[0], kFlagInclusive | agg);
+      if (lane == 0) st_relaxed_u64(&status[0], kFlagInclusive | agg);
     } else {
-      if (lane == 0) st_release_u64(&status[tile], kFlagAggregate | agg);
+      if (lane == 0) st_relaxed_u64(&status[tile], kFlagAggregate | agg);
       int64_t base = (int64_t)tile - 1;
       while (true) {
         const int64_t idx = base - (int64_t)lane;
-        unsigned long long s = idx >= 0 ? ld_acquire_u64(&status[idx]) : kFlagInclusive;
+        unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : kFlagInclusive;
         while (__any_sync(kFull, (s >> 62) == 0)) {
-          if ((s >> 62) == 0) s = ld_acquire_u64(&status[idx]);
+          if ((s >> 62) == 0) s = ld_relaxed_u64(&status[idx]);
         }
         const uint32_t incl_mask = __ballot_sync(kFull, (s >> 62) == 2);
         unsigned long long v = s & kValueMask;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads)
         excl += warp_sum(v);
         base -= 32;
       }
-      if (lane == 0) st_release_u64(&status[tile], kFlagInclusive | (excl + agg));
+      if (lane == 0) st_relaxed_u64(&status[tile], kFlagInclusive | (excl + agg));
     }
     if (lane == 0) sm.exclusive = excl;
   }

@@ -1,0 +1,114 @@
+"""Multi-rank orchestration of paper_2605_10390_b200.dist on CPU: gloo process
+groups (world size 2, 3, 4), one process per rank, 127.0.0.1 rendezvous.
+
+The local steps are injected (OracleOps below, built from the oracle in tests/
+only); the collectives, split sizes, output ranges and the byte-level all-to-all
+are exactly dist.py's.  The concatenation of every rank's output slice must equal
+the single-process oracle sort of the union of the shards.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleOps:
+    """CPU stand-ins for the library calls, computed by the oracle (tests only)."""
+
+    def histogram_u16(self, keys):
+        import oracle
+        return torch.from_numpy(oracle.histogram_u16(keys.numpy()).astype(np.int64))
+
+    def exclusive_scan(self, hist):
+        import oracle
+        return torch.from_numpy(oracle.exclusive_scan(hist.numpy().astype(np.uint64)).astype(np.int64))
+
+    def expand_u16(self, prefix, begin, end):
+        import oracle
+        P = prefix.numpy().astype(np.uint64)
+        C = np.diff(P)
+        return torch.from_numpy(oracle.reconstruct_counts_u16(C, begin, end))
+
+    def sort_keys(self, keys):
+        import oracle
+        return torch.from_numpy(oracle.sort_u16(keys.numpy()))
+
+    def send_counts(self, hist_all, g):
+        import oracle
+        return torch.from_numpy(oracle.send_counts(hist_all.numpy().astype(np.uint64), g).astype(np.int64))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def shard_bounds(n_total, world, rank, uneven):
+    if not uneven:
+        return (n_total * rank) // world, (n_total * (rank + 1)) // world
+    # deliberately uneven shards, including an empty one when world > 2
+    cuts = [0] + sorted({(n_total * (3 * r + 1)) // (3 * world) for r in range(1, world)}) + [n_total]
+    while len(cuts) < world + 1:
+        cuts.insert(1, 0)
+    return cuts[rank], cuts[rank + 1]
+
+
+CASES = [(mode, d, uneven) for mode in ("B", "A")
+         for d, uneven in (("uniform", False), ("zipf", True), ("const", False), ("sortedswap", True))]
+N_TOTAL = 50_003
+
+
+def worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    import datagen
+    from paper_2605_10390_b200 import dist as fsdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for ci, (mode, dist_name, uneven) in enumerate(CASES):
+            b, e = shard_bounds(N_TOTAL, world, rank, uneven)
+            full = datagen.gen_u16(dist_name, N_TOTAL, seed=3)
+            shard = torch.from_numpy(full[b:e].copy())
+            out, (ob, oe) = fsdist.sort_keys_u16(shard, mode=mode, ops=OracleOps())
+            np.save(os.path.join(outdir, f"out_{ci}_{rank}.npy"), out.numpy())
+            np.save(os.path.join(outdir, f"range_{ci}_{rank}.npy"), np.array([ob, oe], dtype=np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_distributed_sort_matches_oracle(tmp_path, world):
+    """Modes A and B, four distributions (uneven and empty shards included)."""
+    import datagen
+    import oracle
+    mp.start_processes(worker, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for ci, (mode, dist_name, uneven) in enumerate(CASES):
+        outs = [np.load(tmp_path / f"out_{ci}_{r}.npy") for r in range(world)]
+        ranges = [tuple(np.load(tmp_path / f"range_{ci}_{r}.npy")) for r in range(world)]
+        # exact equal-count partition (ledger 23): rank d owns [floor(dN/G), floor((d+1)N/G))
+        assert ranges == [((N_TOTAL * d) // world, (N_TOTAL * (d + 1)) // world) for d in range(world)], (mode, dist_name)
+        for (b, e), o in zip(ranges, outs):
+            assert o.size == e - b
+        want = oracle.sort_u16(datagen.gen_u16(dist_name, N_TOTAL, seed=3))
+        np.testing.assert_array_equal(np.concatenate(outs), want, err_msg=f"{mode} {dist_name} world={world}")
+
+
+def test_output_range_helper():
+    from paper_2605_10390_b200.dist import output_range
+    n = 17
+    ranges = [output_range(r, 4, n) for r in range(4)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    assert all(ranges[i][1] == ranges[i + 1][0] for i in range(3))
+    assert sorted(e - b for b, e in ranges) == [4, 4, 4, 5]
