@@ -55,7 +55,7 @@ def launches(path):
     for r in rows[hdr + 1:]:
         if len(r) > vi:
             v = float(r[vi].replace(",", ""))
-            v = v / 1000.0 if r[ui] == "nsecond" else v  # -> us
+            v = v / 1000.0 if r[ui] in ("nsecond", "ns") else (v * 1000.0 if r[ui] in ("msecond", "ms") else v)  # -> us
             per[short(r[ki])].append(v)
     return per
 
