@@ -89,7 +89,7 @@ U16Layout u16_layout(uint64_t n, bool with_prefix) {
   size_t off = 0;
   L.spill_off = off;
   off = align_up(off + sizeof(uint64_t) * kHistBins);
-  L.slice_status_off = off;
+  L.slice_tot_off = off;
   off = align_up(off + sizeof(uint64_t) * kHistSlices);
   L.partials_off = off;
   off = align_up(off + sizeof(uint32_t) * kHistWords * (size_t)L.grid);
@@ -162,17 +162,17 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
   cudaStream_t s = (cudaStream_t)stream;
   char* t = (char*)temp;
   auto* spill = (unsigned long long*)(t + L.spill_off);
-  auto* slice_status = (unsigned long long*)(t + L.slice_status_off);
+  auto* slice_tot = (uint64_t*)(t + L.slice_tot_off);
   auto* partials = (uint32_t*)(t + L.partials_off);
   auto* prefix = (uint64_t*)(t + L.prefix_off);
   phase_event(0, s);
   phase_event(1, s);
   cudaError_t e;
-  if ((e = launch_hist16(keys_in, n, partials, spill, nullptr, 0, 0, prefix, slice_status, L.grid, s)) !=
+  if ((e = launch_hist16(keys_in, n, partials, spill, nullptr, 0, 0, prefix, slice_tot, L.grid, s)) !=
       cudaSuccess)
     return cuda_fail(e, "fs_sort_keys_u16: hist16 (histogram + merge + scan)");
   phase_event(2, s);
-  if ((e = launch_expand16(prefix, kHistBins, 0, n, keys_out, s)) != cudaSuccess)
+  if ((e = launch_expand16_two_level(prefix, slice_tot, 0, n, keys_out, s)) != cudaSuccess)
     return cuda_fail(e, "fs_sort_keys_u16: expand16");
   phase_event(3, s);
   return finish(s, "fs_sort_keys_u16");
@@ -201,10 +201,9 @@ fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint6
     return fail(FS_ERR_INVALID_ARGUMENT, "temp overlaps keys or hist");
   char* t = (char*)temp;
   auto* spill = (unsigned long long*)(t + L.spill_off);
-  auto* slice_status = (unsigned long long*)(t + L.slice_status_off);
   auto* partials = (uint32_t*)(t + L.partials_off);
   cudaError_t e;
-  if ((e = launch_hist16(keys, n, partials, spill, hist, nb, accumulate ? 1 : 0, nullptr, slice_status, L.grid, s)) !=
+  if ((e = launch_hist16(keys, n, partials, spill, hist, nb, accumulate ? 1 : 0, nullptr, nullptr, L.grid, s)) !=
       cudaSuccess)
     return cuda_fail(e, "fs_histogram_u16: hist16 (histogram + merge)");
   return finish(s, "fs_histogram_u16");

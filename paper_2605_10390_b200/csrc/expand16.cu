@@ -7,10 +7,19 @@
 // Restricted to global positions [out_begin, out_end) so a rank of the
 // multi-GPU path writes only its own range (SURVEY.md §8(e) Mode B).
 //
+// The prefix P comes in one of two forms:
+//  * global (fs_expand_u16): P[0..nbins] as given by the caller;
+//  * two-level (the fused sort): P[v] = L[v] + B[v >> 9] where L holds the
+//    slice-local exclusive prefixes written by the histogram kernel and B the
+//    exclusive scan of its 128 slice totals, computed here by every CTA (the
+//    last step of GetIndex, Alg. 3, folded into this kernel's first search
+//    round, so the histogram kernel needs no cross-slice pass).
+//
 // B200 design: HBM-write bound (2 B per key).
 // Each CTA owns an output tile of 32,768 keys (64 KB).  The first and last bin
-// touching the tile are found by a block-parallel search of P (L2-resident):
-// one round over 256 coarse points, one round over the 256 points between them
+// touching the tile are found by a block-parallel search (L2-resident data):
+// one round over 256 coarse points (global form) or the 128 slice bases
+// (two-level form), one round over the <= 512 points between them
 // (__syncthreads_count does the comparisons).  The tile's slice of P is staged
 // in shared memory as 32-bit offsets relative to the tile; each thread emits 8
 // keys per 16-byte streaming store (consecutive lanes -> consecutive 16 B) and
@@ -27,12 +36,33 @@ constexpr int kThreads = 256;
 constexpr int kVecPerThread = 16;
 constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 32,768 keys = 64 KB of output
 constexpr int kSliceCap = 4096;                                    // staged P entries
+constexpr int kSliceShift = 9;                                     // two-level: 512-bin slices
+constexpr int kNumSlices = 65536 >> kSliceShift;                   // 128
+static_assert(kNumSlices == kHistSlices, "slice layout shared with hist16.cu");
 
-// Thread-level binary search over global P: largest v in [lo, hi) with P[v] <= o, given P[lo] <= o.
-FS_DEVINL uint64_t thread_last_le(const uint64_t* __restrict__ P, uint64_t lo, uint64_t hi, uint64_t o) {
+// P[v] for v in [0, nbins]: global array, or slice-local prefix + slice base.
+template <bool kTwoLevel>
+struct PrefixView {
+  const uint64_t* P;          // global P[0..nbins] or slice-local L[0..nbins)
+  const uint64_t* base;       // two-level: shared-memory B[0..128] (B[128] = total)
+  uint64_t nbins;
+  FS_DEVINL uint64_t operator()(uint64_t v) const {
+    if (!kTwoLevel) return __ldcg(P + v);
+    return v >= nbins ? base[kNumSlices] : __ldcg(P + v) + base[v >> kSliceShift];
+  }
+  // P at a coarse-grid point; two-level grid points are slice starts (L = 0 there).
+  FS_DEVINL uint64_t coarse(uint64_t v) const {
+    if (!kTwoLevel) return __ldcg(P + v);
+    return base[v >> kSliceShift];
+  }
+};
+
+// Thread-level binary search: largest v in [lo, hi) with P(v) <= o, given P(lo) <= o.
+template <class View>
+FS_DEVINL uint64_t thread_last_le(const View& P, uint64_t lo, uint64_t hi, uint64_t o) {
   while (hi - lo > 1) {
     const uint64_t mid = lo + (hi - lo) / 2;
-    if (__ldcg(P + mid) <= o) lo = mid; else hi = mid;
+    if (P(mid) <= o) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -53,38 +83,66 @@ FS_DEVINL uint32_t advance(const uint32_t* rel, uint32_t j, uint32_t hi, uint32_
   return lo;
 }
 
-// Block-wide: largest v < nbins with P[v] <= o for two positions at once, in two
-// rounds of loads (256-way coarse, then fine).  All threads get the results.
-FS_DEVINL void block_last_le2(const uint64_t* __restrict__ P, uint64_t nbins, uint64_t o_a, uint64_t o_b,
+// Block-wide: largest v < nbins with P(v) <= o for two positions at once, in two
+// rounds: a coarse grid of `cs`-spaced points, then the points between them.
+template <class View>
+FS_DEVINL void block_last_le2(const View& P, uint64_t nbins, uint64_t cs, uint64_t o_a, uint64_t o_b,
                               uint64_t& v_a, uint64_t& v_b) {
   const uint32_t tid = threadIdx.x;
-  const uint64_t cs = (nbins + kThreads - 1) / kThreads;  // coarse stride (<= 256 for nbins <= 65536)
   const uint64_t ci = (uint64_t)tid * cs;
-  uint64_t p = ci < nbins ? __ldcg(P + ci) : ~0ull;
-  const uint64_t c_a = (uint64_t)__syncthreads_count(p <= o_a) - 1;  // P[0] = 0 <= o
+  const uint64_t p = ci < nbins ? P.coarse(ci) : ~0ull;
+  const uint64_t c_a = (uint64_t)__syncthreads_count(p <= o_a) - 1;  // P(0) = 0 <= o
   const uint64_t c_b = (uint64_t)__syncthreads_count(p <= o_b) - 1;
-  const uint64_t fa = c_a * cs + tid, fb = c_b * cs + tid;
-  const bool in_a = tid < cs && fa < nbins, in_b = tid < cs && fb < nbins;
-  const uint64_t pa = in_a ? __ldcg(P + fa) : ~0ull;
-  const uint64_t pb = in_b ? __ldcg(P + fb) : ~0ull;
-  v_a = c_a * cs + (uint64_t)__syncthreads_count(pa <= o_a) - 1;
-  v_b = c_b * cs + (uint64_t)__syncthreads_count(pb <= o_b) - 1;
+  uint32_t n_a = 0, n_b = 0;
+  for (uint64_t j = tid; j < cs; j += kThreads) {  // cs <= 512: at most two rounds per thread
+    const uint64_t fa = c_a * cs + j, fb = c_b * cs + j;
+    n_a += fa < nbins && P(fa) <= o_a;
+    n_b += fb < nbins && P(fb) <= o_b;
+  }
+  __shared__ uint32_t cnt_sh[2];
+  if (tid == 0) cnt_sh[0] = cnt_sh[1] = 0;
+  __syncthreads();
+  if (n_a) atomicAdd(&cnt_sh[0], n_a);
+  if (n_b) atomicAdd(&cnt_sh[1], n_b);
+  __syncthreads();
+  v_a = c_a * cs + cnt_sh[0] - 1;
+  v_b = c_b * cs + cnt_sh[1] - 1;
 }
 
-__global__ void __launch_bounds__(kThreads)
-    k_expand16(const uint64_t* __restrict__ P, uint64_t nbins, uint64_t pos0, uint64_t nvec,
-               uint16_t* __restrict__ out_body, uint64_t out_begin, uint64_t head, uint64_t tail_pos,
+template <bool kTwoLevel>
+__global__ void __launch_bounds__(kThreads, 8)
+    k_expand16(const uint64_t* __restrict__ P, const uint64_t* __restrict__ slice_tot, uint64_t nbins, uint64_t pos0,
+               uint64_t nvec, uint16_t* __restrict__ out_body, uint64_t out_begin, uint64_t head, uint64_t tail_pos,
                uint64_t tail_n, uint16_t* __restrict__ out) {
   __shared__ uint32_t rel[kSliceCap];
+  __shared__ uint64_t base_sh[kNumSlices + 1];
+  __shared__ uint64_t wtot[kThreads / 32];
   const uint32_t tid = threadIdx.x;
   // Programmatic dependent launch: everything above overlaps the producer's tail;
   // P is read only after the producer grid has completed.
   cudaGridDependencySynchronize();
 
+  if (kTwoLevel) {  // slice bases: exclusive scan of the 128 slice totals
+    const uint64_t t = tid < kNumSlices ? __ldcg(slice_tot + tid) : 0ull;
+    const uint64_t inc = warp_inclusive_scan<uint64_t>(t);
+    if ((tid & 31) == 31) wtot[tid >> 5] = inc;
+    __syncthreads();
+    uint64_t off = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      if (w < (int)(tid >> 5)) off += wtot[w];
+      all += wtot[w];
+    }
+    if (tid < kNumSlices) base_sh[tid] = off + inc - t;
+    if (tid == 0) base_sh[kNumSlices] = all;
+    __syncthreads();
+  }
+  const PrefixView<kTwoLevel> Pv{P, base_sh, nbins};
+
   // Unaligned head/tail keys (< 8 each): one per thread in CTA 0.
   if (blockIdx.x == 0 && tid < head + tail_n) {
     const uint64_t j = tid < head ? out_begin + tid : tail_pos + (tid - head);
-    out[j - out_begin] = (uint16_t)thread_last_le(P, 0, nbins, j);
+    out[j - out_begin] = (uint16_t)thread_last_le(Pv, 0, nbins, j);
   }
   if (nvec == 0) return;
 
@@ -93,13 +151,16 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t o0 = pos0 + vec0 * 8;  // first global position of the tile
   const uint32_t len = (uint32_t)((vec_end - vec0) * 8);
   uint64_t v_lo, v_hi;
-  block_last_le2(P, nbins, o0, o0 + len - 1, v_lo, v_hi);
+  // Coarse grid: the 128 slice starts (two-level: their P values are the bases
+  // already in shared memory) or 256 evenly spaced points of the global P.
+  block_last_le2(Pv, nbins, kTwoLevel ? (uint64_t)1 << kSliceShift : (nbins + kThreads - 1) / kThreads, o0,
+                 o0 + len - 1, v_lo, v_hi);
   const uint64_t m = v_hi - v_lo + 2;  // P[v_lo .. v_hi+1]
   uint4* dst = reinterpret_cast<uint4*>(out_body) + vec0;
 
   if (m <= (uint64_t)kSliceCap) {
     for (uint32_t j = tid; j < m; j += kThreads) {
-      const uint64_t p = __ldcg(P + v_lo + j);
+      const uint64_t p = Pv(v_lo + j);
       rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
     }
     __syncthreads();
@@ -144,13 +205,13 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t l = q * 8;
       if (l >= len) break;
       uint32_t packed[4] = {0, 0, 0, 0};
-      uint64_t v = thread_last_le(P, v_lo, v_hi + 1, o0 + l);
-      uint64_t run_end = __ldcg(P + v + 1);
+      uint64_t v = thread_last_le(Pv, v_lo, v_hi + 1, o0 + l);
+      uint64_t run_end = Pv(v + 1);
       for (int e = 0; e < 8; ++e) {
         const uint64_t pos = o0 + l + e;
         if (pos >= run_end) {
-          v = thread_last_le(P, v + 1, v_hi + 1, pos);
-          run_end = __ldcg(P + v + 1);
+          v = thread_last_le(Pv, v + 1, v_hi + 1, pos);
+          run_end = Pv(v + 1);
         }
         packed[e / 2] |= ((uint32_t)v & 0xFFFFu) << (16 * (e & 1));
       }
@@ -159,10 +220,9 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-}  // namespace
-
-cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
-                            uint16_t* out, cudaStream_t s) {
+template <bool kTwoLevel>
+cudaError_t launch(const uint64_t* prefix, const uint64_t* slice_tot, uint64_t nbins, uint64_t out_begin,
+                   uint64_t out_end, uint16_t* out, cudaStream_t s) {
   const uint64_t n = out_end - out_begin;
   if (n == 0) return cudaSuccess;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(out);
@@ -185,8 +245,20 @@ cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   uint16_t* body = out + head;
-  return cudaLaunchKernelEx(&cfg, k_expand16, prefix, nbins, pos0, nvec, body, out_begin, head, tail_pos, tail_n,
-                            out);
+  return cudaLaunchKernelEx(&cfg, k_expand16<kTwoLevel>, prefix, slice_tot, nbins, pos0, nvec, body, out_begin, head,
+                            tail_pos, tail_n, out);
+}
+
+}  // namespace
+
+cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
+                            uint16_t* out, cudaStream_t s) {
+  return launch<false>(prefix, nullptr, nbins, out_begin, out_end, out, s);
+}
+
+cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64_t* slice_tot, uint64_t out_begin,
+                                      uint64_t out_end, uint16_t* out, cudaStream_t s) {
+  return launch<true>(slice_prefix, slice_tot, kHistBins, out_begin, out_end, out, s);
 }
 
 }  // namespace fs

@@ -35,12 +35,13 @@
 //    sees an all-equal vector switches to an aggregating mode (one +8 per
 //    thread or one +256 per warp instead of same-address atomics); the check is
 //    sampled every 4th group while not aggregating.
-//  * Prologue zeroes the spill array and slice flags (grid-strided) and the
-//    grid synchronises once, so the call needs no memset node.
+//  * Prologue zeroes the spill array (grid-strided) and the grid synchronises
+//    once, so the call needs no memset node.
 //  * Tail: each CTA flushes its partial (L2-resident), grid sync, then 128
 //    slices of 512 bins are merged (16 row groups x 64 columns of 16-byte
-//    loads), and each slice's exclusive base is the sum of all earlier slice
-//    totals read in parallel (one round of loads, no serial lookback chain).
+//    loads).  For the sort, each slice writes its local exclusive prefix and
+//    its total; the 128-entry scan of the totals is done by the expansion
+//    kernel's first search round (no cross-slice pass here).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -48,12 +49,31 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef FS_HIST_TRACE
+// Debug-only phase timestamps (scripts/microbench/hist_trace.cu builds this file
+// with -DFS_HIST_TRACE); compiled out of libfractalsort.so.
+__device__ unsigned long long g_hist_trace[256][8];
+#define FS_TRACE(i)                                                                    \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      unsigned long long t_;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+      g_hist_trace[blockIdx.x][i] = t_;                                                \
+    }                                                                                  \
+  } while (0)
+#else
+#define FS_TRACE(i) \
+  do {              \
+  } while (0)
+#endif
+
 namespace fs {
 namespace {
 
 constexpr int kThreads = 1024;
 constexpr int kUnroll = 2;                  // 128-bit vectors per thread per group
 constexpr uint32_t kHotMask = 0x80008000u;  // either 16-bit half >= 2^15
+constexpr int kMaxGrid = 1024;              // CTAs (one per SM): the merge loops over rows
 static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violated");
 
 FS_DEVINL void spill_word(uint32_t* sh, uint32_t w, unsigned long long* spill) {
@@ -135,8 +155,8 @@ struct HistArgs {
   uint64_t* hist_out;                  // optional: C written (+=) for v < nbins_out
   uint64_t nbins_out;
   int accumulate;
-  uint64_t* prefix;                    // optional: 65537 exclusive prefix (the sort path)
-  unsigned long long* slice_status;    // kSlices words (zeroed in the prologue)
+  uint64_t* prefix;                    // optional: slice-local exclusive prefix L[65536] (the sort path)
+  uint64_t* slice_tot;                 // with prefix: the 128 slice totals
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
@@ -144,13 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem_v4);
   const uint32_t tid = threadIdx.x;
   cg::grid_group grid = cg::this_grid();
+  FS_TRACE(0);
 
   // ---------------- prologue: zero the local tree, the spill array and the flags
 #pragma unroll
   for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
   for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins; i += gridDim.x * kThreads) a.spill[i] = 0;
-  if (blockIdx.x == 0 && tid < kSlices) a.slice_status[tid] = 0;
   grid.sync();
+  FS_TRACE(1);
 
   // ---------------- stage 1: local compressed histogram
   // Unaligned head and ragged tail (< 8 + 7 keys) go to the last CTA, one key per thread.
@@ -200,12 +221,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     if (add8(sh, q) & kHotMask) recheck8(sh, q, a.spill);
   }
   __syncthreads();
+  FS_TRACE(2);
 
   // Flush the local tree: the first step of the two-step merge.
   uint4* dst = reinterpret_cast<uint4*>(a.partials + (uint64_t)blockIdx.x * kHistWords);
 #pragma unroll
   for (int j = 0; j < kHistWords / 4 / kThreads; ++j) dst[tid + j * kThreads] = smem_v4[tid + j * kThreads];
+  FS_TRACE(3);
   grid.sync();
+  FS_TRACE(4);
   // The dependent kernel (expansion) may start launching; it waits for this
   // grid's completion before reading P (programmatic dependent launch).
   cudaTriggerProgrammaticLaunchCompletion();
@@ -246,7 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
       if (a.hist_out && bin < a.nbins_out) a.hist_out[bin] = a.accumulate ? a.hist_out[bin] + c : c;
     }
     if (a.prefix) {
-      // slice-local exclusive scan; the slice's base is added in stage 2
+      // slice-local exclusive scan L[v] and the slice total; the expansion
+      // kernel adds the slice bases (two-level prefix, see expand16.cu)
       const unsigned long long inc = warp_inclusive_scan<unsigned long long>(c);
       if ((tid & 31) == 31 && tid < kSliceBins) wsum[tid >> 5] = inc;
       __syncthreads();
@@ -258,36 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
         tot += t;
       }
       if (tid < kSliceBins) a.prefix[bin] = off + inc - c;
-      if (tid == 0) st_relaxed_u64(&a.slice_status[slice], kFlagAggregate | tot);
+      if (tid == 0) a.slice_tot[slice] = tot;
     }
     __syncthreads();
   }
-  if (!a.prefix) return;
-
-  // ---------------- stage 2: exclusive scan across slices (GetIndex, Alg. 3)
-  // Each slice's base is the sum of all earlier slice totals, read in parallel
-  // (128 slices: one round of loads instead of a serial lookback chain).
-  __shared__ unsigned long long base_sh[kThreads / 32];
-  for (int slice = blockIdx.x; slice < kSlices; slice += G) {
-    unsigned long long t = 0;
-    if ((int)tid < slice) {
-      unsigned long long s;
-      do { s = ld_relaxed_u64(&a.slice_status[tid]); } while ((s >> 62) == 0);
-      t = s & kValueMask;
-    }
-    t = warp_sum(t);
-    if ((tid & 31) == 0) base_sh[tid >> 5] = t;
-    __syncthreads();
-    unsigned long long base = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) base += base_sh[w];
-    const uint32_t bin = slice * kSliceBins + tid;
-    if (tid < kSliceBins) {
-      a.prefix[bin] += base;
-      if (bin == kHistBins - 1) a.prefix[kHistBins] = base + (ld_relaxed_u64(&a.slice_status[slice]) & kValueMask);
-    }
-    __syncthreads();
-  }
+  FS_TRACE(5);
+  FS_TRACE(6);
 }
 
 }  // namespace
@@ -296,12 +297,13 @@ int hist16_grid(uint64_t n) {
   const uint64_t want = (n + 65535) / 65536;  // keep >= 64K keys per CTA: the flush is 128 KB
   const uint64_t sms = (uint64_t)device_info().sm_count;
   uint64_t g = want < sms ? want : sms;
+  if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
   return g ? (int)g : 1;
 }
 
 cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill,
                           uint64_t* hist_out, uint64_t nbins_out, int accumulate, uint64_t* prefix,
-                          unsigned long long* slice_status, int grid, cudaStream_t s) {
+                          uint64_t* slice_tot, int grid, cudaStream_t s) {
   static_assert(kHistWords % (4 * kThreads) == 0, "flush mapping");
   static_assert(kRowGroups * kSliceBins * 4 + 16 * 8 <= kHistWords * 4, "merge smem");
   constexpr int smem = kHistWords * 4;
@@ -321,7 +323,7 @@ cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, 
   a.nbins_out = nbins_out;
   a.accumulate = accumulate;
   a.prefix = prefix;
-  a.slice_status = slice_status;
+  a.slice_tot = slice_tot;
   void* args[] = {&a};
   // Cooperative launch: all CTAs co-resident (one per SM), so grid.sync() is safe.
   return cudaLaunchCooperativeKernel((const void*)k_hist16, dim3(grid), dim3(kThreads), args, smem, s);

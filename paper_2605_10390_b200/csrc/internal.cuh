@@ -14,7 +14,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // zeroing by the caller: the histogram kernel zeroes its spill and flags.
 struct U16Layout {
   int grid = 1;
-  size_t spill_off = 0, slice_status_off = 0, partials_off = 0, prefix_off = 0, total = 0;
+  size_t spill_off = 0, slice_tot_off = 0, partials_off = 0, prefix_off = 0, total = 0;
 };
 U16Layout u16_layout(uint64_t n, bool with_prefix);
 

@@ -20,14 +20,15 @@ const DeviceInfo& device_info();
 constexpr int kHistBins = 65536;
 constexpr int kHistWords = kHistBins / 2;  // two 16-bit counters per 32-bit word
 constexpr int kHistSlices = 128;            // 512-bin merge/scan slices
-int hist16_grid(uint64_t n);
+int hist16_grid(uint64_t n);  // min(#SM, ceil(n / 65536))
 // Cooperative launch, one CTA per SM: local histograms -> partials, grid sync,
 // merge (C written to hist_out if non-null, += when accumulate), and, when
-// prefix != nullptr, the exclusive scan P[0..65536].  spill (65536 u64) and
-// slice_status (kHistSlices u64) are scratch; the kernel zeroes them itself.
+// prefix != nullptr, the two-level prefix: prefix[v] = sum of C over the bins of
+// v's 512-bin slice below v, slice_tot[s] = total of slice s (kHistSlices).
+// spill (65536 u64) is scratch; the kernel zeroes it itself.
 cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, unsigned long long* spill,
                           uint64_t* hist_out, uint64_t nbins_out, int accumulate, uint64_t* prefix,
-                          unsigned long long* slice_status, int grid, cudaStream_t s);
+                          uint64_t* slice_tot, int grid, cudaStream_t s);
 
 // ---------------------------------------------------------------- scan.cu
 constexpr int kScanTileBins = 256;
@@ -46,6 +47,9 @@ cudaError_t launch_merge_scan(const uint32_t* partials, int parts, const unsigne
 // Count-expansion of prefix into out for global positions [out_begin, out_end) (stage 3).
 cudaError_t launch_expand16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
                             uint16_t* out, cudaStream_t s);
+// Same from the two-level prefix written by launch_hist16 (65,536 bins).
+cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64_t* slice_tot, uint64_t out_begin,
+                                      uint64_t out_end, uint16_t* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- partition.cu
 cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
