@@ -59,6 +59,9 @@ __device__ unsigned long long g_hist_trace[256][8];
       unsigned long long t_;                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
       g_hist_trace[blockIdx.x][i] = t_;                                                \
+      unsigned smid_;                                                                  \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                               \
+      g_hist_trace[blockIdx.x][7] = smid_;                                             \
     }                                                                                  \
   } while (0)
 #else

@@ -14,13 +14,15 @@
 //     histogram has a single non-empty bin is skipped; the ping-pong parity of
 //     every executed pass is fixed on the device so the last pass lands in the
 //     caller's output (no host synchronisation).
-//  3. k_onesweep (per digit): tiles of 4096 keys taken in order from an atomic
-//     ticket; warp-level ranking with __match_any_sync (input order preserved:
-//     item-major, lane-minor within a warp chunk, warps in order); per-tile
-//     digit counts published to a 64-bit status word per (tile, digit)
-//     [flag:2 | pass tag:6 | value:56]; decoupled lookback, one thread per digit;
-//     keys (and values) reordered through shared memory so each digit's run is
-//     written with consecutive addresses.
+//  3. k_onesweep (per digit): tiles of 3072 keys (256 threads x 12 items, 4
+//     CTAs per SM) taken in order from an atomic ticket; warp-level ranking with
+//     an 8-ballot multisplit (input order preserved: item-major, lane-minor
+//     within a warp chunk, warps in order; match.any measured ~10x slower);
+//     per-tile digit counts published to a 64-bit status word per (tile, digit)
+//     [flag:2 | pass tag:6 | value:56] with relaxed stores; decoupled lookback,
+//     one thread per digit, 8 predecessors fetched per round; keys (and values)
+//     reordered through shared memory so each digit's run is written with
+//     consecutive addresses.
 #include "common.cuh"
 #include "internal.cuh"
 #include "kernels.cuh"
@@ -115,7 +117,7 @@ struct PassSmem {
 };
 
 template <typename K, bool kHasValues>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 4)
     k_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kX,
                uint32_t* __restrict__ vX, K* __restrict__ kY, uint32_t* __restrict__ vY, uint64_t n, int pass,
                const Plan* __restrict__ plan, unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket) {
@@ -147,13 +149,8 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const uint64_t idx = chunk0 + 32 * i + lane;
-    if (idx < n) {
-      key[i] = __ldcs(src_k + idx);
-      if (kHasValues) val[i] = __ldcs(src_v + idx);
-    } else {
-      key[i] = 0;
-      if (kHasValues) val[i] = 0;
-    }
+    key[i] = idx < n ? __ldcs(src_k + idx) : K(0);
+    if (kHasValues) val[i] = idx < n ? __ldcs(src_v + idx) : 0u;
   }
 
   // ---- warp-level stable ranking
@@ -202,13 +199,27 @@ __global__ void __launch_bounds__(kThreads, 3)
     st_relaxed_u64(st, kStFlagInc | tag | cnt);
   } else {
     st_relaxed_u64(st, kStFlagAgg | tag | cnt);
+    // Look back kLook predecessors per round: their status loads are independent,
+    // so a round costs one L2 round trip instead of kLook.  Walk them in order
+    // (nearest first), summing aggregates until an inclusive prefix.
+    constexpr int kLook = 8;
     int64_t t = (int64_t)tile - 1;
-    while (true) {
-      const unsigned long long s = ld_relaxed_u64(status + (uint64_t)t * kRadix + d);
-      if ((s & (0x3Full << kTagShift)) != tag || (s >> 62) == 0) continue;  // not yet published
-      excl += s & kStValue;
-      if ((s >> 62) == 2 || t == 0) break;
-      --t;
+    bool done = false;
+    while (!done) {
+      unsigned long long sv[kLook];
+#pragma unroll
+      for (int j = 0; j < kLook; ++j)
+        sv[j] = t - j >= 0 ? ld_relaxed_u64(status + (uint64_t)(t - j) * kRadix + d) : (kStFlagInc | tag);
+#pragma unroll
+      for (int j = 0; j < kLook; ++j) {
+        if (done) break;
+        unsigned long long s = sv[j];
+        while ((s & (0x3Full << kTagShift)) != tag || (s >> 62) == 0)  // not yet published: wait for it
+          s = ld_relaxed_u64(status + (uint64_t)(t - j) * kRadix + d);
+        excl += s & kStValue;
+        done = (s >> 62) == 2;
+      }
+      t -= kLook;
     }
     st_relaxed_u64(st, kStFlagInc | tag | (excl + cnt));
   }

@@ -33,6 +33,10 @@ int main(){
     const char* nm[7]={"start","prologue+sync","mainloop end","flush end","sync2","merge end","scan end"};
     for(int i=0;i<7;i++){ std::vector<double> v; for(int c=0;c<G;c++) v.push_back((tr[c][i]-t0)/1e3); std::sort(v.begin(),v.end());
       printf("  %-14s min %7.2f  med %7.2f  max %7.2f us\n",nm[i],v[0],v[v.size()/2],v.back()); }
+    if(rep==3){ // per-CTA main-loop duration vs SM id
+      printf("cta smid mainloop_us\n");
+      for(int c=0;c<G;c++) printf("%d %llu %.2f\n", c, tr[c][7], (tr[c][2]-tr[c][1])/1e3);
+    }
   }
   return 0;
 }
