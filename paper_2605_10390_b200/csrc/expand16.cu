@@ -33,8 +33,8 @@ namespace fs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kVecPerThread = 16;
-constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 32,768 keys = 64 KB of output
+constexpr int kVecPerThread = 16;                                  // max 16-byte vectors per thread
+constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 32,768 keys = 64 KB of output (max)
 constexpr int kSliceCap = 4096;                                    // staged P entries
 constexpr int kSliceShift = 9;                                     // two-level: 512-bin slices
 constexpr int kNumSlices = 65536 >> kSliceShift;                   // 128
@@ -109,11 +109,14 @@ FS_DEVINL void block_last_le2(const View& P, uint64_t nbins, uint64_t cs, uint64
   v_b = c_b * cs + cnt_sh[1] - 1;
 }
 
-template <bool kTwoLevel>
+// kVpt: vectors per thread, fixed at compile time (16) for large outputs; 0 means
+// the runtime value `vpt` (small outputs, smaller tiles).
+template <bool kTwoLevel, int kVpt>
 __global__ void __launch_bounds__(kThreads, 8)
     k_expand16(const uint64_t* __restrict__ P, const uint64_t* __restrict__ slice_tot, uint64_t nbins, uint64_t pos0,
                uint64_t nvec, uint16_t* __restrict__ out_body, uint64_t out_begin, uint64_t head, uint64_t tail_pos,
-               uint64_t tail_n, uint16_t* __restrict__ out) {
+               uint64_t tail_n, uint16_t* __restrict__ out, uint32_t vpt_rt) {
+  const uint32_t vpt = kVpt ? (uint32_t)kVpt : vpt_rt;
   __shared__ uint32_t rel[kSliceCap];
   __shared__ uint64_t base_sh[kNumSlices + 1];
   __shared__ uint64_t wtot[kThreads / 32];
@@ -146,8 +149,9 @@ __global__ void __launch_bounds__(kThreads, 8)
   }
   if (nvec == 0) return;
 
-  const uint64_t vec0 = (uint64_t)blockIdx.x * (kTile / 8);
-  const uint64_t vec_end = vec0 + kTile / 8 < nvec ? vec0 + kTile / 8 : nvec;
+  const uint64_t tile_vec = (uint64_t)kThreads * vpt;  // vectors per tile (vpt <= kVecPerThread)
+  const uint64_t vec0 = (uint64_t)blockIdx.x * tile_vec;
+  const uint64_t vec_end = vec0 + tile_vec < nvec ? vec0 + tile_vec : nvec;
   const uint64_t o0 = pos0 + vec0 * 8;  // first global position of the tile
   const uint32_t len = (uint32_t)((vec_end - vec0) * 8);
   uint64_t v_lo, v_hi;
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 8)
     const uint32_t hi = (uint32_t)m - 1;  // searches stay below the sentinel rel[m-1] >= len
     uint32_t j = 0;                       // rel[0] = 0: valid start for every position
 #pragma unroll 4
-    for (int k = 0; k < kVecPerThread; ++k) {
+    for (uint32_t k = 0; k < vpt; ++k) {
       const uint32_t q = k * kThreads + tid;
       const uint32_t l = q * 8;
       if (l >= len) break;
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 8)
   } else {
     // Very sparse tile (more than kSliceCap bins): search P in L2 per position.
 #pragma unroll 1
-    for (int k = 0; k < kVecPerThread; ++k) {
+    for (uint32_t k = 0; k < vpt; ++k) {
       const uint32_t q = k * kThreads + tid;
       const uint32_t l = q * 8;
       if (l >= len) break;
@@ -232,7 +236,12 @@ cudaError_t launch(const uint64_t* prefix, const uint64_t* slice_tot, uint64_t n
   const uint64_t tail_n = n - head - nvec * 8;
   const uint64_t pos0 = out_begin + head;
   const uint64_t tail_pos = pos0 + nvec * 8;
-  uint64_t grid = (nvec * 8 + kTile - 1) / kTile;
+  // 64 KB tiles for large outputs; smaller tiles so that small outputs still
+  // give every SM several CTAs.
+  const uint64_t want = (uint64_t)device_info().sm_count * 4;
+  uint32_t vpt = kVecPerThread;
+  while (vpt > 1 && (nvec + (uint64_t)kThreads * vpt - 1) / ((uint64_t)kThreads * vpt) < want) vpt >>= 1;
+  uint64_t grid = (nvec + (uint64_t)kThreads * vpt - 1) / ((uint64_t)kThreads * vpt);
   if (grid == 0) grid = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -245,8 +254,11 @@ cudaError_t launch(const uint64_t* prefix, const uint64_t* slice_tot, uint64_t n
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   uint16_t* body = out + head;
-  return cudaLaunchKernelEx(&cfg, k_expand16<kTwoLevel>, prefix, slice_tot, nbins, pos0, nvec, body, out_begin, head,
-                            tail_pos, tail_n, out);
+  if (vpt == kVecPerThread)
+    return cudaLaunchKernelEx(&cfg, k_expand16<kTwoLevel, kVecPerThread>, prefix, slice_tot, nbins, pos0, nvec, body,
+                              out_begin, head, tail_pos, tail_n, out, vpt);
+  return cudaLaunchKernelEx(&cfg, k_expand16<kTwoLevel, 0>, prefix, slice_tot, nbins, pos0, nvec, body, out_begin, head,
+                            tail_pos, tail_n, out, vpt);
 }
 
 }  // namespace
