@@ -77,6 +77,7 @@ constexpr int kThreads = 1024;
 constexpr int kUnroll = 2;                  // 128-bit vectors per thread per group
 constexpr uint32_t kHotMask = 0x80008000u;  // either 16-bit half >= 2^15
 constexpr int kMaxGrid = 1024;              // CTAs (one per SM): the merge loops over rows
+constexpr int kSmallGrid = 32;              // up to this many CTAs, the merge of stage 1b is column-per-thread
 static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violated");
 
 FS_DEVINL void spill_word(uint32_t* sh, uint32_t w, unsigned long long* spill) {
@@ -237,8 +238,58 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   // grid's completion before reading P (programmatic dependent launch).
   cudaTriggerProgrammaticLaunchCompletion();
 
-  // ---------------- stage 1b: merge, one 512-bin slice at a time
+  // ---------------- stage 1b: merge
   const int G = gridDim.x;
+  if (G <= kSmallGrid) {
+    // Few CTAs (small n): each thread owns one 8-bin column of one of this
+    // CTA's slices and sums all G rows itself; a slice's 64 columns are two
+    // warps, which scan their 512 bins together.  16 slices per round.
+    __shared__ unsigned long long pair_tot[kThreads / 32];
+    const uint32_t my_slices = (kSlices - blockIdx.x + G - 1) / G;
+    constexpr uint32_t kPerRound = kThreads / kSliceVec;  // 16
+    for (uint32_t r0 = 0; r0 < my_slices; r0 += kPerRound) {
+      const uint32_t s_local = r0 + tid / kSliceVec, c = tid % kSliceVec;
+      const bool active = s_local < my_slices;
+      const uint32_t slice = blockIdx.x + s_local * G;
+      uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (active) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.partials) + (uint64_t)slice * kSliceVec + c;
+#pragma unroll 4
+        for (int g = 0; g < G; ++g) {
+          const uint4 q = __ldcg(src + (uint64_t)g * (kHistWords / 4));
+          acc[0] += q.x & 0xFFFFu; acc[1] += q.x >> 16; acc[2] += q.y & 0xFFFFu; acc[3] += q.y >> 16;
+          acc[4] += q.z & 0xFFFFu; acc[5] += q.z >> 16; acc[6] += q.w & 0xFFFFu; acc[7] += q.w >> 16;
+        }
+      }
+      unsigned long long cnt[8], tot = 0;
+      const uint32_t bin0 = slice * kSliceBins + c * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = active ? acc[j] + a.spill[bin0 + j] : 0ull;
+        tot += cnt[j];
+        if (active && a.hist_out && bin0 + j < a.nbins_out)
+          a.hist_out[bin0 + j] = a.accumulate ? a.hist_out[bin0 + j] + cnt[j] : cnt[j];
+      }
+      if (a.prefix) {
+        // exclusive scan over the slice's 64 columns (warps 2k and 2k+1)
+        const unsigned long long inc = warp_inclusive_scan<unsigned long long>(tot);
+        if ((tid & 31) == 31) pair_tot[tid >> 5] = inc;
+        __syncthreads();
+        unsigned long long run = inc - tot + (((tid >> 5) & 1) ? pair_tot[(tid >> 5) - 1] : 0ull);
+        if (active) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            a.prefix[bin0 + j] = run;
+            run += cnt[j];
+          }
+          if (c == kSliceVec - 1) a.slice_tot[slice] = run;
+        }
+        __syncthreads();  // pair_tot is reused by the next round
+      }
+    }
+    FS_TRACE(5);
+    return;
+  }
   uint32_t* part = sh;                                                                       // [16][512] u32
   unsigned long long* wsum = reinterpret_cast<unsigned long long*>(sh + kRowGroups * kSliceBins);  // [16]
   const uint32_t col = tid % kSliceVec, rg = tid / kSliceVec;
