@@ -87,8 +87,8 @@ U16Layout u16_layout(uint64_t n, bool with_prefix) {
   U16Layout L;
   L.grid = hist16_grid(n);
   size_t off = 0;
-  L.spill_off = off;
-  off = align_up(off + sizeof(uint64_t) * kHistBins);
+  L.spill_off = off;  // spill u64[65536], then the dynamic-work counter (kernels.cuh kHistSpillWords)
+  off = align_up(off + sizeof(uint64_t) * kHistSpillWords);
   L.slice_tot_off = off;
   off = align_up(off + sizeof(uint64_t) * kHistSlices);
   L.partials_off = off;

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   // ---------------- prologue: zero the local tree, the spill array and the flags
 #pragma unroll
   for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
-  for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins; i += gridDim.x * kThreads) a.spill[i] = 0;
+  for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins + 1; i += gridDim.x * kThreads) a.spill[i] = 0;
   grid.sync();
   FS_TRACE(1);
 
@@ -189,17 +189,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   }
   const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(a.keys + a.head);
   const uint64_t nvec = a.nvec;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  uint64_t i = (uint64_t)blockIdx.x * kThreads + tid;
-  // The bound is tested on the warp's last lane so the whole warp iterates
-  // together (warp collectives inside).
-  const uint64_t warp_tail = 31 - lane_id();
+  // Work is split into groups of kUnroll x 1024 vectors (16,384 keys).  Most
+  // groups are assigned statically (grid-strided); the last 1/8 are handed out
+  // dynamically in warp-sized chunks (2,048 keys) from a global counter,
+  // because SMs run the atomic-bound loop at rates ~8% apart (hist_trace:
+  // per-CTA loop 115-125 us on 2^28 keys).  Per-warp tickets need no CTA
+  // barrier, so no warp waits on another's loads.
+  constexpr uint64_t kGroupVec = (uint64_t)kUnroll * kThreads;
+  constexpr int kChunkIters = 4;
+  constexpr uint64_t kChunkVec = (uint64_t)kChunkIters * kUnroll * 32;
+  static_assert(kGroupVec % kChunkVec == 0, "chunks tile the groups");
+  const uint64_t ngroups = nvec / kGroupVec;
+  const uint64_t nstatic = ngroups - ngroups / 8;
   bool agg = false;
   uint32_t phase = 0;
-  for (; i + warp_tail + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+  // v[u] = p[u * stride]; the whole warp calls this together.
+  auto process = [&](const uint4* p, uint32_t stride) {
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream_v4(vec + i + u * stride);
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream_v4(p + u * stride);
     if (agg || phase == 0) {
       bool runs = false;
 #pragma unroll
@@ -219,8 +227,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
         for (int u = 0; u < kUnroll; ++u) recheck8(sh, v[u], a.spill);
       }
     }
+  };
+  for (uint64_t g = blockIdx.x; g < nstatic; g += gridDim.x) process(vec + g * kGroupVec + tid, kThreads);
+  {
+    unsigned int* work = reinterpret_cast<unsigned int*>(a.spill + kHistBins);
+    const uint64_t dyn0 = nstatic * kGroupVec;
+    const uint64_t nchunks = (ngroups * kGroupVec - dyn0) / kChunkVec;
+    const uint32_t lane = lane_id();
+    for (;;) {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(work, 1u);
+      c = __shfl_sync(kFull, c, 0);
+      if (c >= nchunks) break;
+      const uint4* p = vec + dyn0 + (uint64_t)c * kChunkVec + lane;
+#pragma unroll 1
+      for (int j = 0; j < kChunkIters; ++j) process(p + j * kUnroll * 32, 32);
+    }
   }
-  for (; i < nvec; i += stride) {
+  // Vectors after the last full group (< 2,048).
+  for (uint64_t i = ngroups * kGroupVec + (uint64_t)blockIdx.x * kThreads + tid; i < nvec;
+       i += (uint64_t)gridDim.x * kThreads) {
     const uint4 q = ld_stream_v4(vec + i);
     if (add8(sh, q) & kHotMask) recheck8(sh, q, a.spill);
   }
@@ -296,21 +322,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   for (int slice = blockIdx.x; slice < kSlices; slice += G) {
     uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint4* src = reinterpret_cast<const uint4*>(a.partials) + (uint64_t)slice * kSliceVec + col;
-    int g = rg;
-    for (; g + 3 * kRowGroups < G; g += 4 * kRowGroups) {
-      uint4 q[4];
+    // the spill of this thread's bin, fetched together with the partial rows
+    const unsigned long long spilled = tid < kSliceBins ? __ldcg(a.spill + slice * kSliceBins + tid) : 0ull;
+    // All of this thread's rows (G <= 160: one batch) are loaded before any is
+    // summed, so the merge costs one L2 round trip instead of ceil(G / 64).
+    constexpr int kBatch = 10;
+    for (int g0 = rg; g0 < G; g0 += kBatch * kRowGroups) {
+      uint4 q[kBatch];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = __ldcg(src + (uint64_t)(g + u * kRowGroups) * (kHistWords / 4));
+      for (int u = 0; u < kBatch; ++u) {
+        const int g = g0 + u * kRowGroups;
+        q[u] = g < G ? __ldcg(src + (uint64_t)g * (kHistWords / 4)) : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kBatch; ++u) {
         acc[0] += q[u].x & 0xFFFFu; acc[1] += q[u].x >> 16; acc[2] += q[u].y & 0xFFFFu; acc[3] += q[u].y >> 16;
         acc[4] += q[u].z & 0xFFFFu; acc[5] += q[u].z >> 16; acc[6] += q[u].w & 0xFFFFu; acc[7] += q[u].w >> 16;
       }
-    }
-    for (; g < G; g += kRowGroups) {
-      const uint4 q = __ldcg(src + (uint64_t)g * (kHistWords / 4));
-      acc[0] += q.x & 0xFFFFu; acc[1] += q.x >> 16; acc[2] += q.y & 0xFFFFu; acc[3] += q.y >> 16;
-      acc[4] += q.z & 0xFFFFu; acc[5] += q.z >> 16; acc[6] += q.w & 0xFFFFu; acc[7] += q.w >> 16;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) part[rg * kSliceBins + col * 8 + j] = acc[j];
@@ -320,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     if (tid < kSliceBins) {
 #pragma unroll
       for (int r = 0; r < kRowGroups; ++r) c += part[r * kSliceBins + tid];
-      c += a.spill[bin];
+      c += spilled;
       if (a.hist_out && bin < a.nbins_out) a.hist_out[bin] = a.accumulate ? a.hist_out[bin] + c : c;
     }
     if (a.prefix) {

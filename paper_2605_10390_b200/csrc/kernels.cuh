@@ -20,6 +20,7 @@ const DeviceInfo& device_info();
 constexpr int kHistBins = 65536;
 constexpr int kHistWords = kHistBins / 2;  // two 16-bit counters per 32-bit word
 constexpr int kHistSlices = 128;            // 512-bin merge/scan slices
+constexpr int kHistSpillWords = kHistBins + 32;  // spill[65536] + work counter (zeroed by the kernel)
 int hist16_grid(uint64_t n);  // min(#SM, ceil(n / 65536))
 // Cooperative launch, one CTA per SM: local histograms -> partials, grid sync,
 // merge (C written to hist_out if non-null, += when accumulate), and, when

@@ -18,7 +18,7 @@ int main(){
   setvbuf(stdout,NULL,_IONBF,0);
   uint64_t n=1ull<<28; uint16_t* k; uint32_t* part; unsigned long long *sp; uint64_t *st; uint32_t* rw; uint64_t* P;
   int G=fs::hist16_grid(n);
-  cudaMalloc(&k,n*2); cudaMalloc(&part,(size_t)G*131072); cudaMalloc(&sp,65536*8); cudaMalloc(&st,129*8); cudaMalloc(&rw,1024); cudaMalloc(&P,65537*8);
+  cudaMalloc(&k,n*2); cudaMalloc(&part,(size_t)G*131072); cudaMalloc(&sp,(65536+32)*8); cudaMalloc(&st,129*8); cudaMalloc(&rw,1024); cudaMalloc(&P,65537*8);
   gen<<<1184,256>>>(k,n); cudaDeviceSynchronize();
   for(int rep=0;rep<4;rep++){
     cudaEvent_t a,b; cudaEventCreate(&a); cudaEventCreate(&b);
