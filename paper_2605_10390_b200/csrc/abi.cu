@@ -137,10 +137,10 @@ size_t fs_histogram_u16_temp_bytes(uint64_t n) { return u16_layout(n, false).tot
 size_t fs_exclusive_scan_u64_temp_bytes(uint64_t nbins) {
   return align_up(sizeof(uint64_t) * scan_tiles(nbins ? nbins : 1)) + 256;
 }
-size_t fs_sort_keys_u32_temp_bytes(uint64_t n, int key_bits) { return onesweep_temp_bytes(n, 4, key_bits, false); }
-size_t fs_sort_keys_u64_temp_bytes(uint64_t n, int key_bits) { return onesweep_temp_bytes(n, 8, key_bits, false); }
+size_t fs_sort_keys_u32_temp_bytes(uint64_t n, int key_bits) { return wide_temp_bytes(n, 4, key_bits, false); }
+size_t fs_sort_keys_u64_temp_bytes(uint64_t n, int key_bits) { return wide_temp_bytes(n, 8, key_bits, false); }
 size_t fs_sort_pairs_u64_u32_temp_bytes(uint64_t n, int key_bits) {
-  return onesweep_temp_bytes(n, 8, key_bits, true);
+  return wide_temp_bytes(n, 8, key_bits, true);
 }
 
 fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t n, int key_bits, void* temp,
@@ -281,7 +281,7 @@ static fs_status wide_sort(const char* name, const void* kin, const uint32_t* vi
     return fail(FS_ERR_INVALID_ARGUMENT, "%s: keys misaligned", name);
   if (pairs && (((uintptr_t)vin | (uintptr_t)vout) & 3))
     return fail(FS_ERR_INVALID_ARGUMENT, "%s: values misaligned", name);
-  const size_t need = onesweep_temp_bytes(n, key_bytes, key_bits, pairs);
+  const size_t need = wide_temp_bytes(n, key_bytes, key_bits, pairs);
   if (temp_bytes < need) return fail(FS_ERR_INVALID_ARGUMENT, "%s: temp_bytes %zu < required %zu", name, temp_bytes,
                                      need);
   const size_t kb = (size_t)n * key_bytes, vb = (size_t)n * 4;
@@ -292,7 +292,7 @@ static fs_status wide_sort(const char* name, const void* kin, const uint32_t* vi
       (pairs && (overlaps(temp, need, vin, vb) || overlaps(temp, need, vout, vb))))
     return fail(FS_ERR_INVALID_ARGUMENT, "%s: temp overlaps a data buffer", name);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = onesweep_sort(kin, vin, kout, vout, n, key_bytes, key_bits, temp, temp_bytes, s);
+  cudaError_t e = wide_sort(kin, vin, kout, vout, n, key_bytes, key_bits, temp, temp_bytes, s);
   if (e != cudaSuccess) return cuda_fail(e, name);
   return finish(s, name);
 }

@@ -56,11 +56,13 @@ cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64
 cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                                cudaStream_t s);
 
-// ---------------------------------------------------------------- onesweep.cu
-// LSD radix sort of u32/u64 keys (+ optional u32 values), 8-bit digits.
-size_t onesweep_temp_bytes(uint64_t n, int key_bytes, int key_bits, bool has_values);
-cudaError_t onesweep_sort(const void* keys_in, const uint32_t* vals_in, void* keys_out, uint32_t* vals_out,
-                          uint64_t n, int key_bytes, int key_bits, void* temp, size_t temp_bytes,
-                          cudaStream_t s);
+// ---------------------------------------------------------------- wide.cu
+// Stable sort of u32/u64 keys (+ optional u32 values): trie-binned MSD with a
+// per-bin local sort when every 16-bit bin fits shared memory (decided on the
+// device), else LSD radix with 8-bit digits.
+size_t wide_temp_bytes(uint64_t n, int key_bytes, int key_bits, bool has_values);
+bool wide_uses_msd(uint64_t n, int key_bytes, int key_bits);
+cudaError_t wide_sort(const void* keys_in, const uint32_t* vals_in, void* keys_out, uint32_t* vals_out, uint64_t n,
+                      int key_bytes, int key_bits, void* temp, size_t temp_bytes, cudaStream_t s);
 
 }  // namespace fs

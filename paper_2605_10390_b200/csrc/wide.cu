@@ -1,0 +1,955 @@
+// wide.cu — multi-digit precision scaling for u32/u64 keys and (u64, u32) pairs
+// (config c5).
+//
+// Two bit-identical schemes (the stable sort is unique, ledger 28):
+//
+// (1) Trie-binned MSD (default for n >= 2^22 and key_bits >= 32).  The paper's
+//     high-precision path (§III.G.3, Alg. 5) bins the keys by
+//     the top levels of the compressed trie and then sorts each bin by its
+//     remaining bits (per-bin radix), with the index array I
+//     carried along:
+//       a. k_top16_hist: one read of the keys builds the leaf level of a
+//          16-level compressed trie over the key's top 16 bits (u16 counters
+//          packed two per word in shared memory; overflow
+//          spill as in hist16.cu), merged and scanned into P16 (scan.cu).  The
+//          level-8 counters of that trie (sums of 256 leaves) are the bucket
+//          bounds of the first MSD digit, the leaves those of the second — no
+//          second histogram is needed.
+//       b. k_scatter mode 1: stable scatter by bits [kb-8, kb) into the
+//          temporary buffer; mode 2: stable scatter by bits [kb-16, kb-8)
+//          within each of the 256 first-level segments, into the output.
+//       c. k_local_sort: every 16-bit bin (<= kLocalCap keys) is sorted in
+//          shared memory by its remaining kb-16 bits, stably, in place.
+//     Traffic: 8 (u64 key read) + 3 x 24 = 80 B/pair for c5 (vs 200 for LSD-8).
+// (2) Stable LSD with 8-bit digits (fallback, and small n / narrow keys): one
+//     read builds all digit histograms (k_digit_hist), k_digit_plan scans them
+//     and skips single-bin digits, then one k_scatter (mode 0) per digit.
+//
+// Choice: the MSD path is taken iff every 16-bit bin holds <= kLocalCap keys —
+// decided on the device (k_msd_plan), so nothing synchronises with the host;
+// the kernels of the path not taken return at once.
+//
+// k_scatter (the "histogram, prefix sum and stable scatter phases"):
+// persistent CTAs (2 per SM for pairs) take 4,096-key tiles in order from an
+// atomic ticket; the next tile's keys and values are prefetched into shared
+// memory with bulk copies (TMA) completing on an mbarrier while the current tile
+// is ranked (8-ballot warp multisplit, stable: item-major, lane-minor, warps in
+// order), its digit counts published to a 64-bit status word per (tile, digit)
+// [flag:2 | pass tag:6 | count:56], reordered through shared memory, offset by a
+// decoupled lookback (one thread per digit, 8 predecessors per round, never
+// crossing a segment start) and written with consecutive addresses per digit.
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "tma.cuh"
+
+namespace fs {
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 256;
+constexpr int kMaxPasses = 8;
+
+// ---- k_scatter geometry
+constexpr int kSThreads = 256;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kSItems = 16;
+constexpr int kSTile = kSThreads * kSItems;  // 4,096 keys per tile
+constexpr int kSlack = 8;                    // 16-byte alignment slack of a tile buffer (elements)
+static_assert(kSThreads == kRadix, "one thread per digit in the lookback");
+
+constexpr unsigned long long kStFlagAgg = 1ull << 62;
+constexpr unsigned long long kStFlagInc = 2ull << 62;
+constexpr int kTagShift = 56;
+constexpr unsigned long long kStValue = (1ull << kTagShift) - 1;
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
+// ---- MSD geometry
+constexpr int kTopBits = 16;            // bits binned by the trie (two 8-bit MSD levels)
+constexpr int kSegs = 256;              // first-level segments
+constexpr int kLocalThreads = 512;
+constexpr int kLocalWarps = kLocalThreads / 32;
+constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in shared memory
+constexpr int kIdxBits = 14;            // local index bits of the composite key
+static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
+constexpr int kCountBitsMax = 13;       // local counting digit (<= 8,192 groups)
+constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
+constexpr uint64_t kMsdMinN = 1ull << 22;
+
+struct LsdPlan {
+  uint64_t base[kMaxPasses][kRadix];  // exclusive digit offsets
+  uint32_t skip[kMaxPasses];
+  uint32_t exec_index[kMaxPasses];    // 1-based index among executed passes
+  uint32_t executed;                  // E
+};
+
+struct MsdPlan {
+  uint32_t use_msd;           // 1: MSD kernels run, LSD kernels return; 0: the reverse
+  uint32_t l2_tiles;          // tiles of the level-2 pass
+  uint32_t seg_tile0[kSegs + 1];
+  uint64_t seg_begin[kSegs + 1];
+};
+
+template <typename K>
+FS_DEVINL uint32_t digit_of(K key, int shift) {
+  return (uint32_t)(key >> shift) & (kRadix - 1);
+}
+
+FS_DEVINL bool lsd_enabled(const MsdPlan* msd) { return msd == nullptr || msd->use_msd == 0; }
+
+// ================================================================ histograms
+// LSD: all digit histograms from one read of the keys.
+template <typename K>
+__global__ void __launch_bounds__(512)
+    k_digit_hist(const K* __restrict__ keys, uint64_t n, int passes, unsigned long long* __restrict__ hist,
+                 const MsdPlan* __restrict__ msd) {
+  if (!lsd_enabled(msd)) return;
+  __shared__ uint32_t sh[kMaxPasses * kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = __ldcs(keys + i);
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p)
+      if (p < passes) atomicAdd(&sh[p * kRadix + digit_of(k, p * kRadixBits)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+__global__ void __launch_bounds__(kRadix)
+    k_digit_plan(const unsigned long long* __restrict__ hist, uint64_t n, int passes, LsdPlan* __restrict__ plan,
+                 const MsdPlan* __restrict__ msd) {
+  if (!lsd_enabled(msd)) return;
+  __shared__ uint32_t skip_sh[kMaxPasses];
+  __shared__ unsigned long long wsum[kRadix / 32];
+  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  if (d < kMaxPasses) skip_sh[d] = 0;
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const unsigned long long c = hist[p * kRadix + d];
+    if (c == n) skip_sh[p] = 1;  // every key has this digit: the pass is the identity
+    const unsigned long long inc = warp_inclusive_scan<unsigned long long>(c);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned long long off = 0;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    plan->base[p][d] = off + inc - c;
+    __syncthreads();
+  }
+  if (d == 0) {
+    uint32_t e = 0;
+    for (int p = 0; p < kMaxPasses; ++p) {
+      const uint32_t s = p < passes ? skip_sh[p] : 1u;
+      plan->skip[p] = s;
+      if (!s) ++e;
+      plan->exec_index[p] = s ? 0u : e;
+    }
+    plan->executed = e;
+  }
+}
+
+// MSD: leaf level of the 16-level compressed trie over the top 16 key bits.
+// Same counter layout and overflow protocol as hist16.cu: u16 counters packed
+// two per word; an add whose returned word has a half >= 2^15 exchanges the word
+// with 0 into the u64 spill.  Every add is checked at once, so a counter stays
+// below 2^15 + 32 warps x 64 + 1024 < 65,536.
+constexpr uint32_t kHotMask = 0x80008000u;
+
+FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long long* spill) {
+  const uint32_t w = bin >> 1;
+  const uint32_t old = atomicAdd(&sh[w], (bin & 1u) ? (cnt << 16) : cnt);
+  if (old & kHotMask) {
+    const uint32_t x = atomicExch(&sh[w], 0u);
+    if (x & 0xFFFFu) atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
+    if (x >> 16) atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(1024, 1)
+    k_top16_hist(const K* __restrict__ keys, uint64_t n, int shift, uint32_t* __restrict__ partials,
+                 unsigned long long* __restrict__ spill, const MsdPlan* __restrict__ unused) {
+  (void)unused;
+  constexpr int kPerVec = 16 / sizeof(K);
+  constexpr int kUnroll = 4;
+  extern __shared__ uint4 sm4[];
+  uint32_t* sh = reinterpret_cast<uint32_t*>(sm4);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  for (int i = tid; i < kHistWords / 4; i += 1024) sm4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
+  uint64_t head = ((16 - (addr & 15)) & 15) / sizeof(K);
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / kPerVec;
+  const uint64_t tail0 = head + nvec * kPerVec;
+  if (blockIdx.x == gridDim.x - 1) {  // unaligned head and ragged tail, one key per thread
+    for (uint64_t t = tid; t < head + (n - tail0); t += 1024) {
+      const uint64_t idx = t < head ? t : tail0 + (t - head);
+      top_add(sh, (uint32_t)(keys[idx] >> shift) & 0xFFFFu, 1u, spill);
+    }
+  }
+  const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(keys + head);
+  const uint64_t stride = (uint64_t)gridDim.x * 1024;
+  // whole warps iterate together (warp vote inside)
+  const uint64_t first = (uint64_t)blockIdx.x * 1024 + (tid & ~31u);
+  for (uint64_t w0 = first; w0 < nvec; w0 += kUnroll * stride) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t i = w0 + u * stride + lane;
+      v[u] = i < nvec ? ld_stream_v4(vec + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t i = w0 + u * stride + lane;
+      if (w0 + u * stride >= nvec) break;  // warp-uniform
+      const bool valid = i < nvec;
+      K k[kPerVec];
+      memcpy(k, &v[u], 16);
+      uint32_t b[kPerVec];
+      bool same = valid;
+#pragma unroll
+      for (int j = 0; j < kPerVec; ++j) b[j] = (uint32_t)(k[j] >> shift) & 0xFFFFu;
+      const uint32_t b0 = __shfl_sync(kFull, b[0], 0);
+#pragma unroll
+      for (int j = 0; j < kPerVec; ++j) same &= b[j] == b0;
+      const uint32_t same_mask = __ballot_sync(kFull, same);
+      if (same_mask == kFull) {  // runs (sorted / low-entropy keys): one add per warp
+        if (lane == 0) top_add(sh, b0, 32u * kPerVec, spill);
+      } else if (valid) {
+#pragma unroll
+        for (int j = 0; j < kPerVec; ++j) top_add(sh, b[j], 1u, spill);
+      }
+    }
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(partials + (uint64_t)blockIdx.x * kHistWords);
+  for (int i = tid; i < kHistWords / 4; i += 1024) dst[i] = sm4[i];
+}
+
+// MSD plan: whether every 16-bit bin fits the local sort, and the tiles of the
+// level-2 pass (segments = first-level buckets, bounds from P16).
+__global__ void __launch_bounds__(kSegs)
+    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, MsdPlan* __restrict__ plan) {
+  __shared__ uint32_t wsum[kSegs / 32];
+  __shared__ int too_big;
+  const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
+  if (s == 0) too_big = 0;
+  __syncthreads();
+  uint64_t mx = 0;
+  for (int j = 0; j < 256; ++j) mx = max(mx, (uint64_t)H16[s * 256 + j]);
+  if (mx > (uint64_t)kLocalCap) too_big = 1;
+  const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
+  const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
+  const uint32_t inc = warp_inclusive_scan<uint32_t>(tiles);
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t off = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSegs / 32; ++w) {
+    if (w < (int)warp) off += wsum[w];
+    tot += wsum[w];
+  }
+  plan->seg_tile0[s] = off + inc - tiles;
+  plan->seg_begin[s] = b;
+  if (s == kSegs - 1) {
+    plan->seg_tile0[kSegs] = tot;
+    plan->seg_begin[kSegs] = e;
+    plan->l2_tiles = tot;
+  }
+  __syncthreads();
+  if (s == 0) plan->use_msd = too_big ? 0u : 1u;
+}
+
+// ================================================================ scatter pass
+template <typename K>
+struct ScatterArgs {
+  const K* kin;             // the caller's input
+  const uint32_t* vin;
+  K* kA;                    // the caller's output
+  uint32_t* vA;
+  K* kB;                    // the temporary buffer
+  uint32_t* vB;
+  uint64_t n;
+  int mode;                 // 0: LSD pass `pass`; 1: MSD level 1; 2: MSD level 2
+  int pass;
+  int shift;                // digit = (key >> shift) & 255
+  const LsdPlan* lsd;
+  const MsdPlan* msd;
+  const uint64_t* P16;
+  unsigned long long* status;
+  uint32_t* ticket;
+  unsigned long long tag;   // pass tag << kTagShift
+  uint32_t tiles;           // modes 0, 1: ceil(n / kSTile)
+  int tma;                  // every buffer 16-byte aligned: bulk-copy prefetch
+};
+
+struct TileInfo {
+  uint64_t begin, end, abeg;  // [begin, end) of the source; abeg = bulk-copy start (<= begin)
+  uint32_t tile, seg;
+  uint32_t first;             // first tile of its segment
+  uint32_t pad;
+};
+
+template <typename K, bool kHasValues>
+struct ScatterSmem {
+  K keys[2][kSTile + kSlack];
+  uint32_t vals[2][kHasValues ? kSTile + kSlack : 1];
+  uint32_t whist[kSWarps][kRadix];   // per-warp counts, then per-warp exclusive offsets
+  uint32_t digit_start[kRadix];      // tile-local exclusive scan over digits
+  unsigned long long gofs[kRadix];   // global offset - digit_start
+  uint32_t seg_tile0[kSegs + 1];
+  uint32_t wsum[kSWarps];
+  uint64_t mbar[2];
+  TileInfo info[2];
+};
+
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<ScatterSmem<K, kHasValues>*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+
+  // ---- resolve this pass (uniform across the grid)
+  const K* src_k;
+  const uint32_t* src_v;
+  K* dst_k;
+  uint32_t* dst_v;
+  const uint64_t* base_tab;
+  uint32_t base_ss = 0, base_ds = 1, ntiles;
+  if (a.mode == 0) {
+    if (!lsd_enabled(a.msd) || a.lsd->skip[a.pass]) return;
+    const uint32_t E = a.lsd->executed, e = a.lsd->exec_index[a.pass];
+    const bool dst_is_a = ((E - e) & 1u) == 0;  // the last executed pass lands in the caller's output
+    src_k = e == 1 ? a.kin : (dst_is_a ? a.kB : a.kA);
+    src_v = e == 1 ? a.vin : (dst_is_a ? a.vB : a.vA);
+    dst_k = dst_is_a ? a.kA : a.kB;
+    dst_v = dst_is_a ? a.vA : a.vB;
+    base_tab = a.lsd->base[a.pass];
+    ntiles = a.tiles;
+  } else {
+    if (!a.msd->use_msd) return;
+    if (a.mode == 1) {
+      src_k = a.kin; src_v = a.vin; dst_k = a.kB; dst_v = a.vB;
+      base_tab = a.P16;
+      base_ds = 256;  // level 1: base[d] = P16[d << 8]
+      ntiles = a.tiles;
+    } else {
+      src_k = a.kB; src_v = a.vB; dst_k = a.kA; dst_v = a.vA;
+      base_tab = a.P16;
+      base_ss = 256;  // level 2: base[s][d] = P16[(s << 8) | d]
+      ntiles = a.msd->l2_tiles;
+    }
+  }
+  const uint64_t n = a.n;
+  const uint64_t n_al = n & ~(uint64_t)3;  // bulk copies never read past this
+
+  // Thread 0: take the next tile, describe it, and (with TMA) start its copy.
+  auto fetch = [&](int buf) {
+    TileInfo t;
+    t.tile = atomicAdd(a.ticket, 1u);
+    t.pad = 0;
+    if (t.tile >= ntiles) {
+      t.tile = kNoTile;
+      t.begin = t.end = t.abeg = 0;
+      t.seg = 0;
+      t.first = 0;
+      sm.info[buf] = t;
+      return;
+    }
+    if (a.mode == 2) {
+      uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sm.seg_tile0[mid] <= t.tile) lo = mid; else hi = mid;
+      }
+      while (lo + 1 < kSegs && sm.seg_tile0[lo + 1] <= t.tile) ++lo;  // skip empty segments
+      const uint64_t sb = __ldcg(&a.msd->seg_begin[lo]), se = __ldcg(&a.msd->seg_begin[lo + 1]);
+      t.seg = lo;
+      t.first = t.tile == sm.seg_tile0[lo];
+      t.begin = sb + (uint64_t)(t.tile - sm.seg_tile0[lo]) * kSTile;
+      t.end = min(t.begin + kSTile, se);
+    } else {
+      t.seg = 0;
+      t.first = t.tile == 0;
+      t.begin = (uint64_t)t.tile * kSTile;
+      t.end = min(t.begin + kSTile, n);
+    }
+    t.abeg = a.tma ? (t.begin & ~(uint64_t)3) : t.begin;
+    sm.info[buf] = t;
+    if (a.tma) {
+      const uint64_t aend = min((t.end + 3) & ~(uint64_t)3, n_al);
+      const uint32_t cnt = aend > t.abeg ? (uint32_t)(aend - t.abeg) : 0u;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&sm.mbar[buf], cnt * (uint32_t)(sizeof(K) + (kHasValues ? 4 : 0)));
+      if (cnt) {
+        bulk_g2s(sm.keys[buf], src_k + t.abeg, cnt * (uint32_t)sizeof(K), &sm.mbar[buf]);
+        if (kHasValues) bulk_g2s(sm.vals[buf], src_v + t.abeg, cnt * 4u, &sm.mbar[buf]);
+      }
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(&sm.mbar[0], 1);
+    mbar_init(&sm.mbar[1], 1);
+    mbar_fence_init();
+  }
+  if (a.mode == 2)
+    for (int i = tid; i <= kSegs; i += kSThreads) sm.seg_tile0[i] = __ldcg(&a.msd->seg_tile0[i]);
+  for (int i = tid; i < kSWarps * kRadix; i += kSThreads) (&sm.whist[0][0])[i] = 0;
+  __syncthreads();
+  if (tid == 0) fetch(0);
+  __syncthreads();
+
+  const int shift = a.shift;
+  for (uint32_t it = 0;; ++it) {
+    const int cur = it & 1;
+    const TileInfo ti = sm.info[cur];
+    if (ti.tile == kNoTile) break;
+    if (tid == 0) fetch(cur ^ 1);  // prefetch the next tile while this one is processed
+    K* kbuf = sm.keys[cur];
+    uint32_t* vbuf = kHasValues ? sm.vals[cur] : nullptr;
+    const uint32_t len = (uint32_t)(ti.end - ti.begin);
+    const uint32_t off = (uint32_t)(ti.begin - ti.abeg);
+    if (a.tma) {
+      mbar_wait(&sm.mbar[cur], (it >> 1) & 1u);
+      // keys past the last 16-byte boundary of the array (< 4): plain loads
+      const uint64_t covered = max(min((ti.end + 3) & ~(uint64_t)3, n_al), ti.begin);
+      if (covered < ti.end) {
+        const uint32_t e0 = (uint32_t)(covered - ti.begin);
+        if (tid < len - e0) {
+          kbuf[off + e0 + tid] = src_k[covered + tid];
+          if (kHasValues) vbuf[off + e0 + tid] = src_v[covered + tid];
+        }
+        __syncthreads();
+      }
+    } else {
+      for (uint32_t e = tid; e < len; e += kSThreads) {
+        kbuf[e] = src_k[ti.begin + e];
+        if (kHasValues) vbuf[e] = src_v[ti.begin + e];
+      }
+      __syncthreads();
+    }
+
+    // ---- items: warp w holds tile elements [512 w, 512 w + 512), item i of lane l = 512 w + 32 i + l
+    K key[kSItems];
+    uint32_t val[kHasValues ? kSItems : 1];
+    const uint32_t e0 = warp * 32 * kSItems + lane;
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      const uint32_t e = e0 + 32 * i;
+      key[i] = e < len ? kbuf[off + e] : K(0);
+      if (kHasValues) val[i] = e < len ? vbuf[off + e] : 0u;
+    }
+
+    // ---- warp-level stable ranking (8-ballot multisplit)
+    uint32_t rank[kSItems];
+    uint32_t* wh = sm.whist[warp];
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      const bool valid = e0 + 32 * i < len;
+      const uint32_t d = digit_of(key[i], shift);
+      uint32_t peers = __ballot_sync(kFull, valid);
+#pragma unroll
+      for (int b = 0; b < kRadixBits; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t vote = __ballot_sync(kFull, bit);
+        peers &= bit ? vote : ~vote;
+      }
+      const uint32_t leader = 31 - __clz(peers);
+      uint32_t old = 0;
+      if (valid && lane == leader) {
+        old = wh[d];
+        wh[d] = old + __popc(peers);
+      }
+      old = __shfl_sync(kFull, old, leader);
+      rank[i] = old + __popc(peers & lanemask_lt());
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- tile digit counts and per-warp offsets (thread = digit); publish
+    const uint32_t d = tid;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kSWarps; ++w) {
+      const uint32_t c = sm.whist[w][d];
+      sm.whist[w][d] = cnt;
+      cnt += c;
+    }
+    unsigned long long* st = a.status + (uint64_t)ti.tile * kRadix + d;
+    if (ti.first) st_relaxed_u64(st, kStFlagInc | a.tag | cnt);
+    else st_relaxed_u64(st, kStFlagAgg | a.tag | cnt);
+    const uint32_t inc = warp_inclusive_scan<uint32_t>(cnt);
+    if (lane == 31) sm.wsum[warp] = inc;
+    __syncthreads();
+    uint32_t woff = 0;
+#pragma unroll
+    for (int w = 0; w < kSWarps; ++w)
+      if (w < (int)warp) woff += sm.wsum[w];
+    sm.digit_start[d] = woff + inc - cnt;
+    __syncthreads();
+
+    // ---- reorder through shared memory (the tile's input buffer becomes the stage)
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      if (e0 + 32 * i < len) {
+        const uint32_t dd = digit_of(key[i], shift);
+        const uint32_t pos = sm.digit_start[dd] + wh[dd] + rank[i];
+        kbuf[pos] = key[i];
+        if (kHasValues) vbuf[pos] = val[i];
+      }
+    }
+
+    // ---- decoupled lookback over earlier tiles of the segment (thread = digit)
+    unsigned long long excl = 0;
+    if (!ti.first) {
+      constexpr int kLook = 8;
+      int64_t t = (int64_t)ti.tile - 1;
+      bool done = false;
+      while (!done) {
+        unsigned long long sv[kLook];
+#pragma unroll
+        for (int j = 0; j < kLook; ++j)
+          sv[j] = t - j >= 0 ? ld_relaxed_u64(a.status + (uint64_t)(t - j) * kRadix + d) : (kStFlagInc | a.tag);
+#pragma unroll
+        for (int j = 0; j < kLook; ++j) {
+          if (done) break;
+          unsigned long long s = sv[j];
+          while ((s & (0x3Full << kTagShift)) != a.tag || (s >> 62) == 0)  // not yet published
+            s = ld_relaxed_u64(a.status + (uint64_t)(t - j) * kRadix + d);
+          excl += s & kStValue;
+          done = (s >> 62) == 2;
+        }
+        t -= kLook;
+      }
+      st_relaxed_u64(st, kStFlagInc | a.tag | (excl + cnt));
+    }
+    sm.gofs[d] = __ldg(base_tab + (uint64_t)ti.seg * base_ss + (uint64_t)d * base_ds) + excl - sm.digit_start[d];
+    __syncthreads();
+
+    // ---- scatter: consecutive positions of one digit go to consecutive addresses
+    for (uint32_t j = tid; j < len; j += kSThreads) {
+      const K k = kbuf[j];
+      const uint64_t dst = sm.gofs[digit_of(k, shift)] + j;
+      dst_k[dst] = k;
+      if (kHasValues) dst_v[dst] = vbuf[j];
+    }
+    for (int i = tid; i < kSWarps * kRadix; i += kSThreads) (&sm.whist[0][0])[i] = 0;
+    __syncthreads();  // the stage (this buffer) is free for the prefetch after next
+  }
+}
+
+// If every LSD pass was skipped (all keys share every digit), the output is the input.
+template <typename K, bool kHasValues>
+__global__ void k_copy_if_identity(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+                                   uint32_t* __restrict__ vout, uint64_t n, const LsdPlan* __restrict__ plan,
+                                   const MsdPlan* __restrict__ msd) {
+  if (!lsd_enabled(msd) || plan->executed != 0) return;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    kout[i] = kin[i];
+    if (kHasValues) vout[i] = vin[i];
+  }
+}
+
+// ================================================================ local sort
+// One CTA per 16-bit bin b = [P16[b], P16[b+1]) of the output (in place): the
+// per-bin sort of Alg. 5 ("sort_bin") by the remaining
+// R = key_bits - 16 bits, stable.  Keys become composites c = low_R(key) << 14 | i
+// (i = arrival index inside the bin), all distinct, so ordering composites is
+// the stable order.
+//  fast path: counting sort by the top `cb` of the R bits (cb = ceil(log2 m),
+//    <= 13; groups of ~1 key) with shared atomics, then each group (<= 32 keys)
+//    insertion-sorted by composite;
+//  slow path (a group > 32 keys: low-entropy bins): stable LSD over the varying
+//    8-bit digits of the R bits on the permutation (warp multisplit ranks).
+// Output: keys[b0 + j] = (b << R) | (c_j >> 14), vals[b0 + j] = vals_in[b0 + i_j].
+struct LocalSmemLayout {
+  static constexpr int ck = 0;                                           // u64[kLocalCap]
+  static constexpr int perm = ck + kLocalCap * 8;                        // u16[kLocalCap]
+  static constexpr int scratch = perm + kLocalCap * 2;                   // counters | perm_b + whist
+  static constexpr int perm_b = scratch;                                 // u16[kLocalCap]
+  static constexpr int whist = scratch + kLocalCap * 2;                  // u16[16][256]
+  static constexpr int scratch_end =
+      scratch + (kLocalCap * 2 + kLocalWarps * kRadix * 2 > (1 << kCountBitsMax) * 2
+                     ? kLocalCap * 2 + kLocalWarps * kRadix * 2
+                     : (1 << kCountBitsMax) * 2);
+  static constexpr int total = scratch_end;
+};
+
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kLocalThreads, 2)
+    k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
+                 const MsdPlan* __restrict__ msd) {
+  if (!msd->use_msd) return;
+  const uint32_t bkt = blockIdx.x;
+  const uint64_t b0 = __ldg(P16 + bkt);
+  const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
+  if (m <= 1) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* ck = reinterpret_cast<uint64_t*>(smem_raw + LocalSmemLayout::ck);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::perm);
+  uint32_t* cntw = reinterpret_cast<uint32_t*>(smem_raw + LocalSmemLayout::scratch);
+  uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cntw);
+  __shared__ uint32_t heavy;
+  __shared__ uint32_t wtot[kLocalWarps];
+  __shared__ unsigned long long or_all, and_all;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t low_mask = R >= 64 ? ~0ull : ((1ull << R) - 1);
+
+  // counting digit: top cb of the R bits, cb = ceil(log2 m) capped
+  int cb = 32 - __clz(m - 1);
+  cb = min(cb, min(kCountBitsMax, R));
+  const uint32_t ngroups = 1u << cb;
+  const uint32_t nwords = (ngroups + 1) >> 1;
+  const int cshift = kIdxBits + R - cb;
+
+  if (tid == 0) heavy = 0;
+  for (uint32_t w = tid; w < nwords; w += kLocalThreads) cntw[w] = 0;
+  for (uint32_t i = tid; i < m; i += kLocalThreads)
+    ck[i] = (((uint64_t)keys[b0 + i] & low_mask) << kIdxBits) | i;
+  __syncthreads();
+
+  // ---- histogram of the counting digit (u16 counters packed two per word; m < 2^16)
+  for (uint32_t i = tid; i < m; i += kLocalThreads) {
+    const uint32_t g = (uint32_t)(ck[i] >> cshift) & (ngroups - 1);
+    atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
+  }
+  __syncthreads();
+
+  // ---- exclusive scan of the ngroups counters (thread t: words [t*wpt, (t+1)*wpt))
+  {
+    const uint32_t wpt = (nwords + kLocalThreads - 1) / kLocalThreads;  // <= 8
+    const uint32_t w0 = tid * wpt;
+    uint32_t local = 0;
+    for (uint32_t j = 0; j < wpt; ++j)
+      if (w0 + j < nwords) {
+        const uint32_t x = cntw[w0 + j];
+        local += (x & 0xFFFFu) + (x >> 16);
+      }
+    const uint32_t inc = warp_inclusive_scan<uint32_t>(local);
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    uint32_t run = inc - local;
+    for (int w = 0; w < (int)warp; ++w) run += wtot[w];
+    for (uint32_t j = 0; j < wpt; ++j)
+      if (w0 + j < nwords) {
+        const uint32_t x = cntw[w0 + j];
+        const uint32_t lo = run, hi = run + (x & 0xFFFFu);
+        run = hi + (x >> 16);
+        cntw[w0 + j] = lo | (hi << 16);
+      }
+  }
+  __syncthreads();
+
+  // ---- counting scatter of the local indices (order inside a group is fixed below)
+  for (uint32_t i = tid; i < m; i += kLocalThreads) {
+    const uint32_t g = (uint32_t)(ck[i] >> cshift) & (ngroups - 1);
+    const uint32_t old = atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
+    perm[(g & 1u) ? (old >> 16) : (old & 0xFFFFu)] = (uint16_t)i;
+  }
+  __syncthreads();
+
+  // ---- fix-up: insertion sort of every group by composite (cnt16[g] = end of group g)
+  for (uint32_t g = tid; g < ngroups; g += kLocalThreads) {
+    const uint32_t s = g ? cnt16[g - 1] : 0u, e = cnt16[g];
+    if (e - s > (uint32_t)kMaxGroup) {
+      heavy = 1;
+      continue;
+    }
+    for (uint32_t j = s + 1; j < e; ++j) {
+      const uint16_t x = perm[j];
+      const uint64_t kx = ck[x];
+      uint32_t k = j;
+      while (k > s && ck[perm[k - 1]] > kx) {
+        perm[k] = perm[k - 1];
+        --k;
+      }
+      perm[k] = x;
+    }
+  }
+  __syncthreads();
+
+  uint16_t* pfinal = perm;
+  if (heavy) {
+    // ---- slow path: stable LSD over the varying 8-bit digits of the R bits
+    uint16_t* pa = perm;
+    uint16_t* pb = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::perm_b);
+    uint16_t* wh16 = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::whist);  // [warp][digit]
+    if (tid == 0) {
+      or_all = 0;
+      and_all = ~0ull;
+    }
+    __syncthreads();
+    unsigned long long o = 0, an = ~0ull;
+    for (uint32_t i = tid; i < m; i += kLocalThreads) {
+      const uint64_t v = ck[i] >> kIdxBits;
+      o |= v;
+      an &= v;
+      pa[i] = (uint16_t)i;  // arrival order
+    }
+    atomicOr(&or_all, o);
+    atomicAnd(&and_all, an);
+    __syncthreads();
+    const uint64_t varying = or_all ^ and_all;
+    const uint32_t chunk = ((m + kLocalWarps - 1) / kLocalWarps + 31) & ~31u;
+    const uint32_t c0 = min(warp * chunk, m), c1 = min(c0 + chunk, m);
+    for (int sh = 0; sh < R; sh += kRadixBits) {
+      if (((varying >> sh) & 0xFFu) == 0) continue;  // uniform digit: the pass is the identity
+      for (int i = tid; i < kLocalWarps * kRadix; i += kLocalThreads) wh16[i] = 0;
+      __syncthreads();
+      uint16_t* whw = wh16 + warp * kRadix;
+      // pass A: per-warp digit counts over the warp's chunk
+      for (uint32_t j0 = c0; j0 < c1; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const bool valid = j < c1;
+        const uint32_t dg = valid ? (uint32_t)(ck[pa[j]] >> (kIdxBits + sh)) & 0xFFu : 0u;
+        uint32_t peers = __ballot_sync(kFull, valid);
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+          const bool bit = (dg >> b) & 1u;
+          const uint32_t vote = __ballot_sync(kFull, bit);
+          peers &= bit ? vote : ~vote;
+        }
+        if (valid && lane == 31 - __clz(peers)) whw[dg] = (uint16_t)(whw[dg] + __popc(peers));
+        __syncwarp();
+      }
+      __syncthreads();
+      // scan over (digit major, warp minor): thread d < 256 owns digit d
+      if (tid < kRadix) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kLocalWarps; ++w) tot += wh16[w * kRadix + tid];
+        const uint32_t inc = warp_inclusive_scan<uint32_t>(tot);
+        if (lane == 31) wtot[warp] = inc;
+      }
+      __syncthreads();
+      if (tid < kRadix) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kLocalWarps; ++w) tot += wh16[w * kRadix + tid];
+        uint32_t run = warp_inclusive_scan<uint32_t>(tot) - tot;
+        for (int w = 0; w < (int)warp; ++w) run += wtot[w];
+        for (int w = 0; w < kLocalWarps; ++w) {
+          const uint32_t c = wh16[w * kRadix + tid];
+          wh16[w * kRadix + tid] = (uint16_t)run;
+          run += c;
+        }
+      }
+      __syncthreads();
+      // pass B: stable ranks, scatter of the permutation
+      for (uint32_t j0 = c0; j0 < c1; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const bool valid = j < c1;
+        const uint16_t p = valid ? pa[j] : (uint16_t)0;
+        const uint32_t dg = valid ? (uint32_t)(ck[p] >> (kIdxBits + sh)) & 0xFFu : 0u;
+        uint32_t peers = __ballot_sync(kFull, valid);
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+          const bool bit = (dg >> b) & 1u;
+          const uint32_t vote = __ballot_sync(kFull, bit);
+          peers &= bit ? vote : ~vote;
+        }
+        const uint32_t leader = 31 - __clz(peers);
+        uint32_t old = 0;
+        if (valid && lane == leader) {
+          old = whw[dg];
+          whw[dg] = (uint16_t)(old + __popc(peers));
+        }
+        old = __shfl_sync(kFull, old, leader);
+        if (valid) pb[old + __popc(peers & lanemask_lt())] = p;
+        __syncwarp();
+      }
+      __syncthreads();
+      uint16_t* t = pa;
+      pa = pb;
+      pb = t;
+    }
+    pfinal = pa;
+  }
+
+  // ---- write the bin back in sorted order
+  const K top = (K)((uint64_t)bkt << R);
+  for (uint32_t j = tid; j < m; j += kLocalThreads) keys[b0 + j] = top | (K)(ck[pfinal[j]] >> kIdxBits);
+  if (kHasValues) {
+    __syncthreads();  // ck is free: stage the values there
+    uint32_t* sv = reinterpret_cast<uint32_t*>(ck);
+    for (uint32_t i = tid; i < m; i += kLocalThreads) sv[i] = vals[b0 + i];
+    __syncthreads();
+    for (uint32_t j = tid; j < m; j += kLocalThreads) vals[b0 + j] = sv[pfinal[j]];
+  }
+}
+
+// ================================================================ driver
+struct WideLayout {
+  size_t alt_k = 0, alt_v = 0, partials = 0;
+  size_t zero_begin = 0, spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0, zero_end = 0;
+  size_t H16 = 0, P16 = 0, lsd = 0, msd = 0, total = 0;
+  uint64_t tiles = 0, status_tiles = 0;
+  int hgrid = 0;
+  bool use_msd = false;
+};
+
+constexpr int kTickets = 16;  // 0..7 LSD passes, 8 MSD level 1, 9 MSD level 2
+
+WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
+  WideLayout L;
+  const int width = key_bytes * 8;
+  if (key_bits <= 0 || key_bits > width) key_bits = width;
+  L.use_msd = n >= kMsdMinN && key_bits >= 32;
+  L.tiles = (n + kSTile - 1) / kSTile;
+  L.status_tiles = L.tiles + (L.use_msd ? kSegs : 0);
+  const uint64_t sms = (uint64_t)device_info().sm_count;
+  L.hgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 65535) / 65536));
+  size_t off = 0;
+  L.alt_k = off;
+  off = align_up(off + (size_t)n * key_bytes);
+  L.alt_v = off;
+  if (has_values) off = align_up(off + (size_t)n * 4);
+  L.partials = off;
+  if (L.use_msd) off = align_up(off + (size_t)L.hgrid * kHistWords * 4);
+  L.zero_begin = off;  // zeroed by one memset per call
+  L.spill = off;
+  if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * kHistBins);
+  L.scan_status = off;
+  if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * (scan_tiles(kHistBins) + 1));
+  L.tickets = off;
+  off = align_up(off + sizeof(uint32_t) * kTickets);
+  L.digit_hist = off;
+  off = align_up(off + sizeof(unsigned long long) * kMaxPasses * kRadix);
+  L.status = off;
+  off = align_up(off + sizeof(unsigned long long) * kRadix * L.status_tiles);
+  L.zero_end = off;
+  L.H16 = off;
+  if (L.use_msd) off = align_up(off + sizeof(uint64_t) * kHistBins);
+  L.P16 = off;
+  if (L.use_msd) off = align_up(off + sizeof(uint64_t) * (kHistBins + 1));
+  L.lsd = off;
+  off = align_up(off + sizeof(LsdPlan));
+  L.msd = off;
+  off = align_up(off + sizeof(MsdPlan));
+  L.total = off;
+  return L;
+}
+
+template <typename K, bool kHasValues>
+cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int key_bits, void* temp,
+                cudaStream_t s) {
+  const WideLayout L = layout(n, sizeof(K), key_bits, kHasValues);
+  const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+  char* t = (char*)temp;
+  K* alt_k = (K*)(t + L.alt_k);
+  uint32_t* alt_v = kHasValues ? (uint32_t*)(t + L.alt_v) : nullptr;
+  auto* tickets = (uint32_t*)(t + L.tickets);
+  auto* dhist = (unsigned long long*)(t + L.digit_hist);
+  auto* status = (unsigned long long*)(t + L.status);
+  auto* lsd = (LsdPlan*)(t + L.lsd);
+  MsdPlan* msd = L.use_msd ? (MsdPlan*)(t + L.msd) : nullptr;
+  auto* P16 = (uint64_t*)(t + L.P16);
+  const int sms = device_info().sm_count;
+  const bool tma = (((uintptr_t)kin | (uintptr_t)kout | (uintptr_t)alt_k) & 15) == 0 &&
+                   (!kHasValues || (((uintptr_t)vin | (uintptr_t)vout | (uintptr_t)alt_v) & 15) == 0);
+
+  constexpr int ssmem = (int)sizeof(ScatterSmem<K, kHasValues>);
+  cudaError_t e = cudaFuncSetAttribute(k_scatter<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<K, kHasValues>, kSThreads, ssmem)) !=
+      cudaSuccess)
+    return e;
+  const unsigned sgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * std::max(occ, 1),
+                                                                             L.status_tiles));
+  ScatterArgs<K> sa{};
+  sa.kin = kin; sa.vin = vin; sa.kA = kout; sa.vA = vout; sa.kB = alt_k; sa.vB = alt_v;
+  sa.n = n; sa.lsd = lsd; sa.msd = msd; sa.P16 = P16; sa.status = status; sa.tiles = (uint32_t)L.tiles;
+  sa.tma = tma ? 1 : 0;
+
+  phase_event(0, s);
+  if ((e = cudaMemsetAsync(t + L.zero_begin, 0, L.zero_end - L.zero_begin, s)) != cudaSuccess) return e;
+
+  if (L.use_msd) {
+    // ---- trie-binned MSD path
+    const int top_shift = key_bits - kTopBits;
+    auto* partials = (uint32_t*)(t + L.partials);
+    auto* spill = (unsigned long long*)(t + L.spill);
+    auto* scan_status = (unsigned long long*)(t + L.scan_status);
+    auto* H16 = (uint64_t*)(t + L.H16);
+    constexpr int hsmem = kHistWords * 4;
+    if ((e = cudaFuncSetAttribute(k_top16_hist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem)) !=
+        cudaSuccess)
+      return e;
+    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, partials, spill, msd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_merge_scan(partials, L.hgrid, spill, nullptr, kHistBins, H16, kHistBins, 0, P16, scan_status,
+                               (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
+      return e;
+    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, msd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    phase_event(1, s);
+    for (int level = 1; level <= 2; ++level) {
+      sa.mode = level;
+      sa.pass = 0;
+      sa.shift = key_bits - kRadixBits * level;
+      sa.ticket = tickets + 7 + level;
+      sa.tag = (unsigned long long)(8 + level) << kTagShift;
+      k_scatter<K, kHasValues><<<sgrid, kSThreads, ssmem, s>>>(sa);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      phase_event(1 + level, s);
+    }
+    constexpr int lsmem = LocalSmemLayout::total;
+    if ((e = cudaFuncSetAttribute(k_local_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lsmem)) != cudaSuccess)
+      return e;
+    k_local_sort<K, kHasValues><<<kHistBins, kLocalThreads, lsmem, s>>>(kout, vout, P16, key_bits - kTopBits, msd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    phase_event(4, s);
+  }
+
+  // ---- LSD path (the fallback when MSD was planned; every kernel returns at once if MSD ran)
+  uint64_t hgrid = (n + 511) / 512;
+  if (hgrid > (uint64_t)sms * 4) hgrid = (uint64_t)sms * 4;
+  k_digit_hist<K><<<(unsigned)hgrid, 512, 0, s>>>(kin, n, passes, dhist, msd);
+  k_digit_plan<<<1, kRadix, 0, s>>>(dhist, n, passes, lsd, msd);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int ev0 = L.use_msd ? 5 : 1;
+  phase_event(ev0, s);
+  for (int p = 0; p < passes; ++p) {
+    sa.mode = 0;
+    sa.pass = p;
+    sa.shift = p * kRadixBits;
+    sa.ticket = tickets + p;
+    sa.tag = (unsigned long long)(p + 1) << kTagShift;
+    k_scatter<K, kHasValues><<<sgrid, kSThreads, ssmem, s>>>(sa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    phase_event(ev0 + 1 + p, s);
+  }
+  k_copy_if_identity<K, kHasValues><<<(unsigned)(sms * 4), 256, 0, s>>>(kin, vin, kout, vout, n, lsd, msd);
+  phase_event(ev0 + 1 + passes, s);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t wide_temp_bytes(uint64_t n, int key_bytes, int key_bits, bool has_values) {
+  return layout(n, key_bytes, key_bits, has_values).total;
+}
+
+bool wide_uses_msd(uint64_t n, int key_bytes, int key_bits) {
+  return layout(n, key_bytes, key_bits, false).use_msd;
+}
+
+cudaError_t wide_sort(const void* keys_in, const uint32_t* vals_in, void* keys_out, uint32_t* vals_out, uint64_t n,
+                      int key_bytes, int key_bits, void* temp, size_t temp_bytes, cudaStream_t s) {
+  (void)temp_bytes;
+  if (key_bytes == 4)
+    return run<uint32_t, false>((const uint32_t*)keys_in, nullptr, (uint32_t*)keys_out, nullptr, n, key_bits, temp, s);
+  if (vals_in)
+    return run<uint64_t, true>((const uint64_t*)keys_in, vals_in, (uint64_t*)keys_out, vals_out, n, key_bits, temp,
+                               s);
+  return run<uint64_t, false>((const uint64_t*)keys_in, nullptr, (uint64_t*)keys_out, nullptr, n, key_bits, temp, s);
+}
+
+}  // namespace fs

@@ -91,3 +91,83 @@ def test_c5_full_size_invariants(cuda):
     del ko, vo, k, v
     torch.cuda.empty_cache()
     assert oracle.check_pairs_index(kin, kout, vout) == 0
+
+
+# ---------------------------------------------------------------- trie-binned MSD path
+# n >= 2^22 and key_bits >= 32 plan the MSD path (top-16 trie histogram, two
+# stable 8-bit MSD scatters, per-bin local sort); the device falls back to LSD
+# when a 16-bit bin exceeds the local-sort capacity.  Same oracle, bit-exact.
+MSD_N = [1 << 22, (1 << 22) + 3, 5_000_011]
+
+
+@pytest.mark.parametrize("n", MSD_N)
+def test_msd_keys_u64(cuda, n):
+    k = datagen.gen_u64(n, seed=n + 5)
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), oracle.sort_keys_u64(k))
+
+
+@pytest.mark.parametrize("n", MSD_N)
+def test_msd_keys_u32(cuda, n):
+    k = datagen.gen_u32(n, seed=n + 6)
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), oracle.sort_keys_u32(k))
+
+
+@pytest.mark.parametrize("n", MSD_N)
+def test_msd_pairs(cuda, n):
+    k = datagen.gen_u64(n, seed=n + 7)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
+@pytest.mark.parametrize("key_bits", [32, 40, 48, 63])
+def test_msd_pairs_key_bits(cuda, key_bits):
+    n = (1 << 22) + 1
+    k = datagen.gen_u64(n, seed=key_bits + 100, key_bits=key_bits)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda), key_bits=key_bits)
+    ek, ev = oracle.sort_pairs_u64_u32(k, v, key_bits)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
+@pytest.mark.parametrize("distinct_low", [1, 2, 3, 40])
+def test_msd_pairs_heavy_bins(cuda, distinct_low):
+    """Bins that fit shared memory but hold long runs of equal keys: the local
+    sort's slow path (stable LSD on the permutation) must keep arrival order."""
+    n = 1 << 23  # 128 keys per 16-bit bin
+    top = datagen.gen_u64(n, seed=11) & np.uint64(0xFFFF000000000000)
+    low_vals = datagen.gen_u64(distinct_low, seed=12) & np.uint64((1 << 48) - 1)
+    low = low_vals[datagen.gen_u64(n, seed=13) % np.uint64(distinct_low)]
+    k = top | low
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
+def test_msd_fallback_oversize_bin(cuda):
+    """One 16-bit bin above the local-sort capacity: the device takes the LSD path."""
+    n = (1 << 22) + 9
+    k = datagen.gen_u64(n, seed=21)
+    k[: 20_000] = (k[: 20_000] & np.uint64((1 << 48) - 1)) | np.uint64(0x1234 << 48)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
+def test_msd_unaligned_buffers(cuda):
+    """Inputs/outputs not 16-byte aligned: the scatter passes load tiles without bulk copies."""
+    n = (1 << 22) + 5
+    k = datagen.gen_u64(n + 1, seed=31)
+    v = datagen.iota_u32(n + 1)
+    kd, vd = to_dev(k, cuda)[1:], to_dev(v, cuda)[1:]
+    ko, vo = fs.sort_pairs(kd, vd)
+    ek, ev = oracle.sort_pairs_u64_u32(k[1:], v[1:])
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
