@@ -53,12 +53,17 @@ constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 
 // ---- k_scatter geometry
-constexpr int kSThreads = 256;
+#ifndef FS_SCATTER_THREADS  // overridable for scripts/microbench/wide_variants.py
+#define FS_SCATTER_THREADS 256
+#define FS_SCATTER_ITEMS 16
+#define FS_SCATTER_MINB 2
+#endif
+constexpr int kSThreads = FS_SCATTER_THREADS;
 constexpr int kSWarps = kSThreads / 32;
-constexpr int kSItems = 16;
+constexpr int kSItems = FS_SCATTER_ITEMS;
 constexpr int kSTile = kSThreads * kSItems;  // 4,096 keys per tile
 constexpr int kSlack = 8;                    // 16-byte alignment slack of a tile buffer (elements)
-static_assert(kSThreads == kRadix, "one thread per digit in the lookback");
+static_assert(kSThreads >= kRadix, "one thread per digit in the lookback");
 
 constexpr unsigned long long kStFlagAgg = 1ull << 62;
 constexpr unsigned long long kStFlagInc = 2ull << 62;
@@ -74,7 +79,7 @@ constexpr int kLocalWarps = kLocalThreads / 32;
 constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in shared memory
 constexpr int kIdxBits = 14;            // local index bits of the composite key
 static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
-constexpr int kCountBitsMax = 13;       // local counting digit (<= 8,192 groups)
+constexpr int kCountBitsMax = 12;       // local counting digit (<= 4,096 groups)
 constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 constexpr uint64_t kMsdMinN = 1ull << 22;
 
@@ -88,9 +93,31 @@ struct LsdPlan {
 struct MsdPlan {
   uint32_t use_msd;           // 1: MSD kernels run, LSD kernels return; 0: the reverse
   uint32_t l2_tiles;          // tiles of the level-2 pass
+  uint32_t l2_interleave;     // 1: level-2 tickets run across segments (t -> r = t / 256, s = t % 256)
+  uint32_t l2_rmax;           // most tiles in one segment
   uint32_t seg_tile0[kSegs + 1];
   uint64_t seg_begin[kSegs + 1];
 };
+
+// Stable warp multisplit on an 8-bit digit: the lanes of `valid` holding the
+// same digit as this lane.  Written in PTX so each bit costs setp + vote + selp
+// + lop3 (the compiler's form of the same loop costs 6 instructions per bit;
+// scripts/microbench/rank_bench.cu: 14.4 vs 24 cycles per warp-op per SM).
+FS_DEVINL uint32_t match_digit8(uint32_t d, uint32_t valid) {
+  uint32_t peers = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 v, m;\n\t"
+        "and.b32 m, %1, %2;\n\tsetp.ne.u32 p, m, 0;\n\t"
+        "vote.sync.ballot.b32 v, p, 0xffffffff;\n\t"
+        "selp.b32 m, 0, -1, p;\n\t"
+        "lop3.b32 %0, %0, v, m, 0x60;\n\t}"  // peers & (v ^ m): m = ~0 when the bit is 0
+        : "+r"(peers)
+        : "r"(d), "r"(1u << b));
+  }
+  return peers;
+}
 
 template <typename K>
 FS_DEVINL uint32_t digit_of(K key, int shift) {
@@ -159,56 +186,55 @@ __global__ void __launch_bounds__(kRadix)
 // below 2^15 + 32 warps x 64 + 1024 < 65,536.
 constexpr uint32_t kHotMask = 0x80008000u;
 
-FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long long* spill) {
+FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long long* spill, uint32_t* l1spill) {
   const uint32_t w = bin >> 1;
   const uint32_t old = atomicAdd(&sh[w], (bin & 1u) ? (cnt << 16) : cnt);
   if (old & kHotMask) {
     const uint32_t x = atomicExch(&sh[w], 0u);
     if (x & 0xFFFFu) atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
     if (x >> 16) atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
+    if (x) atomicAdd(&l1spill[w >> 7], (x & 0xFFFFu) + (x >> 16));  // this chunk's level-1 count
   }
 }
 
+// CTA b histograms the contiguous chunk [b * chunk, (b+1) * chunk) of the keys,
+// so its flushed partial is the chunk's own 16-bit histogram: the level-1
+// scatter uses the chunks as virtual segments (k_vseg_counts / k_vseg_scan).
 template <typename K>
 __global__ void __launch_bounds__(1024, 1)
-    k_top16_hist(const K* __restrict__ keys, uint64_t n, int shift, uint32_t* __restrict__ partials,
-                 unsigned long long* __restrict__ spill, const MsdPlan* __restrict__ unused) {
-  (void)unused;
+    k_top16_hist(const K* __restrict__ keys, uint64_t n, int shift, uint64_t chunk, uint32_t* __restrict__ partials,
+                 unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill) {
   constexpr int kPerVec = 16 / sizeof(K);
   constexpr int kUnroll = 4;
   extern __shared__ uint4 sm4[];
   uint32_t* sh = reinterpret_cast<uint32_t*>(sm4);
-  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  uint32_t* my_l1spill = l1spill + (uint64_t)blockIdx.x * kRadix;
   for (int i = tid; i < kHistWords / 4; i += 1024) sm4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
+  const uint64_t c0 = (uint64_t)blockIdx.x * chunk, c1 = min(c0 + chunk, n);
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(keys + c0);
   uint64_t head = ((16 - (addr & 15)) & 15) / sizeof(K);
-  if (head > n) head = n;
-  const uint64_t nvec = (n - head) / kPerVec;
-  const uint64_t tail0 = head + nvec * kPerVec;
-  if (blockIdx.x == gridDim.x - 1) {  // unaligned head and ragged tail, one key per thread
-    for (uint64_t t = tid; t < head + (n - tail0); t += 1024) {
-      const uint64_t idx = t < head ? t : tail0 + (t - head);
-      top_add(sh, (uint32_t)(keys[idx] >> shift) & 0xFFFFu, 1u, spill);
-    }
+  if (head > c1 - c0) head = c1 - c0;
+  const uint64_t nvec = (c1 - c0 - head) / kPerVec;
+  const uint64_t tail0 = c0 + head + nvec * kPerVec;
+  for (uint64_t t = tid; t < head + (c1 - tail0); t += 1024) {  // unaligned head and ragged tail
+    const uint64_t idx = t < head ? c0 + t : tail0 + (t - head);
+    top_add(sh, (uint32_t)(keys[idx] >> shift) & 0xFFFFu, 1u, spill, my_l1spill);
   }
-  const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(keys + head);
-  const uint64_t stride = (uint64_t)gridDim.x * 1024;
-  // whole warps iterate together (warp vote inside)
-  const uint64_t first = (uint64_t)blockIdx.x * 1024 + (tid & ~31u);
-  for (uint64_t w0 = first; w0 < nvec; w0 += kUnroll * stride) {
+  const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(keys + c0 + head);
+  for (uint64_t it0 = 0; it0 < nvec; it0 += (uint64_t)kUnroll * 1024) {
     uint4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t i = w0 + u * stride + lane;
+      const uint64_t i = it0 + u * 1024 + tid;
       v[u] = i < nvec ? ld_stream_v4(vec + i) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t i = w0 + u * stride + lane;
-      if (w0 + u * stride >= nvec) break;  // warp-uniform
-      const bool valid = i < nvec;
+      if (it0 + u * 1024 + warp * 32 >= nvec) break;  // warp-uniform (warp vote inside)
+      const bool valid = it0 + u * 1024 + tid < nvec;
       K k[kPerVec];
       memcpy(k, &v[u], 16);
       uint32_t b[kPerVec];
@@ -218,12 +244,11 @@ __global__ void __launch_bounds__(1024, 1)
       const uint32_t b0 = __shfl_sync(kFull, b[0], 0);
 #pragma unroll
       for (int j = 0; j < kPerVec; ++j) same &= b[j] == b0;
-      const uint32_t same_mask = __ballot_sync(kFull, same);
-      if (same_mask == kFull) {  // runs (sorted / low-entropy keys): one add per warp
-        if (lane == 0) top_add(sh, b0, 32u * kPerVec, spill);
+      if (__ballot_sync(kFull, same) == kFull) {  // runs (sorted / low-entropy keys): one add per warp
+        if (lane == 0) top_add(sh, b0, 32u * kPerVec, spill, my_l1spill);
       } else if (valid) {
 #pragma unroll
-        for (int j = 0; j < kPerVec; ++j) top_add(sh, b[j], 1u, spill);
+        for (int j = 0; j < kPerVec; ++j) top_add(sh, b[j], 1u, spill, my_l1spill);
       }
     }
   }
@@ -232,20 +257,60 @@ __global__ void __launch_bounds__(1024, 1)
   for (int i = tid; i < kHistWords / 4; i += 1024) dst[i] = sm4[i];
 }
 
+// Level-1 digit counts of every chunk: cnt[v][d] = sum of the chunk's 256 leaves
+// under level-8 node d (its partial) + what the chunk spilled there.
+__global__ void __launch_bounds__(256)
+    k_vseg_counts(const uint32_t* __restrict__ partials, const uint32_t* __restrict__ l1spill,
+                  uint32_t* __restrict__ cnt, const MsdPlan* __restrict__ msd) {
+  if (!msd->use_msd) return;
+  const uint32_t v = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint4* row = reinterpret_cast<const uint4*>(partials + (uint64_t)v * kHistWords);
+  for (uint32_t d = warp; d < kRadix; d += 8) {
+    const uint4 q = __ldcg(row + d * 32 + lane);  // 128 words = 256 leaves
+    uint32_t x = (q.x & 0xFFFFu) + (q.x >> 16) + (q.y & 0xFFFFu) + (q.y >> 16) + (q.z & 0xFFFFu) + (q.z >> 16) +
+                 (q.w & 0xFFFFu) + (q.w >> 16);
+    x = warp_sum(x);
+    if (lane == 0) cnt[v * kRadix + d] = x + l1spill[v * kRadix + d];
+  }
+}
+
+// vbase[v][d] = P16[d << 8] + sum_{v' < v} cnt[v'][d]: where chunk v's keys of
+// level-1 digit d start in the level-1 output.  One warp per digit.
+__global__ void __launch_bounds__(256)
+    k_vseg_scan(const uint32_t* __restrict__ cnt, int nseg, const uint64_t* __restrict__ P16,
+                uint64_t* __restrict__ vbase, const MsdPlan* __restrict__ msd) {
+  if (!msd->use_msd) return;
+  const uint32_t d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
+  uint64_t run = P16[d << 8];
+  for (int v0 = 0; v0 < nseg; v0 += 32) {
+    const int v = v0 + lane;
+    const uint64_t c = v < nseg ? cnt[v * kRadix + d] : 0ull;
+    const uint64_t inc = warp_inclusive_scan<uint64_t>(c);
+    if (v < nseg) vbase[(uint64_t)v * kRadix + d] = run + inc - c;
+    run += __shfl_sync(kFull, inc, 31);
+  }
+}
+
 // MSD plan: whether every 16-bit bin fits the local sort, and the tiles of the
 // level-2 pass (segments = first-level buckets, bounds from P16).
 __global__ void __launch_bounds__(kSegs)
-    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, MsdPlan* __restrict__ plan) {
+    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint32_t status_cap,
+               MsdPlan* __restrict__ plan) {
   __shared__ uint32_t wsum[kSegs / 32];
+  __shared__ uint32_t rmax;
   __shared__ int too_big;
   const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
-  if (s == 0) too_big = 0;
+  if (s == 0) {
+    too_big = 0;
+    rmax = 0;
+  }
   __syncthreads();
   uint64_t mx = 0;
   for (int j = 0; j < 256; ++j) mx = max(mx, (uint64_t)H16[s * 256 + j]);
   if (mx > (uint64_t)kLocalCap) too_big = 1;
   const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
   const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
+  atomicMax(&rmax, tiles);
   const uint32_t inc = warp_inclusive_scan<uint32_t>(tiles);
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
@@ -263,7 +328,13 @@ __global__ void __launch_bounds__(kSegs)
     plan->l2_tiles = tot;
   }
   __syncthreads();
-  if (s == 0) plan->use_msd = too_big ? 0u : 1u;
+  if (s == 0) {
+    plan->use_msd = too_big ? 0u : 1u;
+    plan->l2_rmax = rmax;
+    // Interleaved tickets keep every segment's lookback one tile deep; worth it
+    // unless the segments are so uneven that most tickets would be holes.
+    plan->l2_interleave = (uint64_t)rmax * kSegs <= (uint64_t)status_cap ? 1u : 0u;
+  }
 }
 
 // ================================================================ scatter pass
@@ -285,32 +356,41 @@ struct ScatterArgs {
   unsigned long long* status;
   uint32_t* ticket;
   unsigned long long tag;   // pass tag << kTagShift
-  uint32_t tiles;           // modes 0, 1: ceil(n / kSTile)
+  uint32_t tiles;           // ceil(n / kSTile)
+  const uint64_t* vbase;    // mode 1: [chunk][digit] level-1 bases (k_vseg_scan)
+  uint32_t l1_nseg;         // mode 1: chunks (virtual segments)
+  uint32_t l1_chunk_tiles;  // mode 1: tiles per chunk
   int tma;                  // every buffer 16-byte aligned: bulk-copy prefetch
 };
 
+// Tile schedule.  Linear: ticket = tile index, the predecessor of a tile is the
+// previous tile (mode 0, and mode 2 with very uneven segments).  Interleaved
+// (modes 1, 2): ticket t is tile r = t / nseg of segment s = t % nseg, so the
+// predecessor in the same segment was issued nseg tickets earlier and has
+// normally published its inclusive prefix: lookbacks stay one round deep
+// instead of trailing a single chain of ~10^5 tiles.  Status word index = ticket.
 struct TileInfo {
   uint64_t begin, end, abeg;  // [begin, end) of the source; abeg = bulk-copy start (<= begin)
-  uint32_t tile, seg;
+  uint32_t tile, seg;         // tile = ticket (kNoTile: no more work)
   uint32_t first;             // first tile of its segment
-  uint32_t pad;
+  uint32_t stride;            // ticket distance to the predecessor in the segment
 };
 
 template <typename K, bool kHasValues>
 struct ScatterSmem {
   K keys[2][kSTile + kSlack];
   uint32_t vals[2][kHasValues ? kSTile + kSlack : 1];
-  uint32_t whist[kSWarps][kRadix];   // per-warp counts, then per-warp exclusive offsets
+  uint16_t whist[kSWarps][kRadix];   // per-warp counts, then per-warp offsets in the tile (<= 4096)
   uint32_t digit_start[kRadix];      // tile-local exclusive scan over digits
   unsigned long long gofs[kRadix];   // global offset - digit_start
   uint32_t seg_tile0[kSegs + 1];
-  uint32_t wsum[kSWarps];
+  uint32_t wsum[kRadix / 32];
   uint64_t mbar[2];
   TileInfo info[2];
 };
 
 template <typename K, bool kHasValues>
-__global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
+__global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterArgs<K> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<ScatterSmem<K, kHasValues>*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -321,7 +401,8 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
   K* dst_k;
   uint32_t* dst_v;
   const uint64_t* base_tab;
-  uint32_t base_ss = 0, base_ds = 1, ntiles;
+  uint32_t base_ss = 0, base_ds = 1, ntiles, nseg = 1;
+  bool inter = false;
   if (a.mode == 0) {
     if (!lsd_enabled(a.msd) || a.lsd->skip[a.pass]) return;
     const uint32_t E = a.lsd->executed, e = a.lsd->exec_index[a.pass];
@@ -336,14 +417,18 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
     if (!a.msd->use_msd) return;
     if (a.mode == 1) {
       src_k = a.kin; src_v = a.vin; dst_k = a.kB; dst_v = a.vB;
-      base_tab = a.P16;
-      base_ds = 256;  // level 1: base[d] = P16[d << 8]
-      ntiles = a.tiles;
+      base_tab = a.vbase;
+      base_ss = 256;  // level 1: base[v][d] = vbase[v * 256 + d]
+      nseg = a.l1_nseg;
+      inter = true;
+      ntiles = a.l1_nseg * a.l1_chunk_tiles;
     } else {
       src_k = a.kB; src_v = a.vB; dst_k = a.kA; dst_v = a.vA;
       base_tab = a.P16;
       base_ss = 256;  // level 2: base[s][d] = P16[(s << 8) | d]
-      ntiles = a.msd->l2_tiles;
+      inter = a.msd->l2_interleave != 0;
+      nseg = inter ? kSegs : 1;
+      ntiles = inter ? kSegs * a.msd->l2_rmax : a.msd->l2_tiles;
     }
   }
   const uint64_t n = a.n;
@@ -352,33 +437,51 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
   // Thread 0: take the next tile, describe it, and (with TMA) start its copy.
   auto fetch = [&](int buf) {
     TileInfo t;
-    t.tile = atomicAdd(a.ticket, 1u);
-    t.pad = 0;
-    if (t.tile >= ntiles) {
-      t.tile = kNoTile;
-      t.begin = t.end = t.abeg = 0;
-      t.seg = 0;
-      t.first = 0;
-      sm.info[buf] = t;
-      return;
-    }
-    if (a.mode == 2) {
-      uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (sm.seg_tile0[mid] <= t.tile) lo = mid; else hi = mid;
+    t.stride = inter ? nseg : 1u;
+    for (;;) {
+      t.tile = atomicAdd(a.ticket, 1u);
+      if (t.tile >= ntiles) {
+        t.tile = kNoTile;
+        t.begin = t.end = t.abeg = 0;
+        t.seg = 0;
+        t.first = 0;
+        sm.info[buf] = t;
+        return;
       }
-      while (lo + 1 < kSegs && sm.seg_tile0[lo + 1] <= t.tile) ++lo;  // skip empty segments
-      const uint64_t sb = __ldcg(&a.msd->seg_begin[lo]), se = __ldcg(&a.msd->seg_begin[lo + 1]);
-      t.seg = lo;
-      t.first = t.tile == sm.seg_tile0[lo];
-      t.begin = sb + (uint64_t)(t.tile - sm.seg_tile0[lo]) * kSTile;
-      t.end = min(t.begin + kSTile, se);
-    } else {
-      t.seg = 0;
-      t.first = t.tile == 0;
-      t.begin = (uint64_t)t.tile * kSTile;
-      t.end = min(t.begin + kSTile, n);
+      uint32_t r;
+      uint64_t sb, se;
+      if (inter) {
+        t.seg = t.tile % nseg;
+        r = t.tile / nseg;
+        if (a.mode == 1) {
+          sb = (uint64_t)t.seg * a.l1_chunk_tiles * kSTile;
+          se = min(sb + (uint64_t)a.l1_chunk_tiles * kSTile, n);
+        } else {
+          if (r >= sm.seg_tile0[t.seg + 1] - sm.seg_tile0[t.seg]) continue;  // hole: segment has fewer tiles
+          sb = __ldcg(&a.msd->seg_begin[t.seg]);
+          se = __ldcg(&a.msd->seg_begin[t.seg + 1]);
+        }
+        if (sb + (uint64_t)r * kSTile >= se) continue;  // hole
+      } else if (a.mode == 2) {
+        uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile (a non-empty segment)
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sm.seg_tile0[mid] <= t.tile) lo = mid; else hi = mid;
+        }
+        t.seg = lo;
+        r = t.tile - sm.seg_tile0[lo];
+        sb = __ldcg(&a.msd->seg_begin[lo]);
+        se = __ldcg(&a.msd->seg_begin[lo + 1]);
+      } else {
+        t.seg = 0;
+        r = t.tile;
+        sb = 0;
+        se = n;
+      }
+      t.first = r == 0;
+      t.begin = sb + (uint64_t)r * kSTile;
+      t.end = min(t.begin + (uint64_t)kSTile, se);
+      break;
     }
     t.abeg = a.tma ? (t.begin & ~(uint64_t)3) : t.begin;
     sm.info[buf] = t;
@@ -401,7 +504,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
   }
   if (a.mode == 2)
     for (int i = tid; i <= kSegs; i += kSThreads) sm.seg_tile0[i] = __ldcg(&a.msd->seg_tile0[i]);
-  for (int i = tid; i < kSWarps * kRadix; i += kSThreads) (&sm.whist[0][0])[i] = 0;
+  for (int i = tid; i < kSWarps * kRadix / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
   __syncthreads();
   if (tid == 0) fetch(0);
   __syncthreads();
@@ -436,7 +539,11 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
       __syncthreads();
     }
 
-    // ---- items: warp w holds tile elements [512 w, 512 w + 512), item i of lane l = 512 w + 32 i + l
+    // Digit threads fetch their global digit base now; it is needed only after the lookback.
+    const uint32_t d = tid;
+    const uint64_t dbase = d < kRadix ? __ldg(base_tab + (uint64_t)ti.seg * base_ss + (uint64_t)d * base_ds) : 0ull;
+
+    // ---- items: warp w holds tile elements [256 w, 256 w + 256), item i of lane l = 256 w + 32 i + l
     K key[kSItems];
     uint32_t val[kHasValues ? kSItems : 1];
     const uint32_t e0 = warp * 32 * kSItems + lane;
@@ -449,23 +556,17 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
 
     // ---- warp-level stable ranking (8-ballot multisplit)
     uint32_t rank[kSItems];
-    uint32_t* wh = sm.whist[warp];
+    uint16_t* wh = sm.whist[warp];
 #pragma unroll
     for (int i = 0; i < kSItems; ++i) {
       const bool valid = e0 + 32 * i < len;
-      const uint32_t d = digit_of(key[i], shift);
-      uint32_t peers = __ballot_sync(kFull, valid);
-#pragma unroll
-      for (int b = 0; b < kRadixBits; ++b) {
-        const bool bit = (d >> b) & 1u;
-        const uint32_t vote = __ballot_sync(kFull, bit);
-        peers &= bit ? vote : ~vote;
-      }
+      const uint32_t dg = digit_of(key[i], shift);
+      const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
       const uint32_t leader = 31 - __clz(peers);
       uint32_t old = 0;
       if (valid && lane == leader) {
-        old = wh[d];
-        wh[d] = old + __popc(peers);
+        old = wh[dg];
+        wh[dg] = (uint16_t)(old + __popc(peers));
       }
       old = __shfl_sync(kFull, old, leader);
       rank[i] = old + __popc(peers & lanemask_lt());
@@ -473,64 +574,78 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
     }
     __syncthreads();
 
-    // ---- tile digit counts and per-warp offsets (thread = digit); publish
-    const uint32_t d = tid;
+    // ---- tile digit counts (thread = digit); publish; per-warp offsets
     uint32_t cnt = 0;
-#pragma unroll
-    for (int w = 0; w < kSWarps; ++w) {
-      const uint32_t c = sm.whist[w][d];
-      sm.whist[w][d] = cnt;
-      cnt += c;
-    }
     unsigned long long* st = a.status + (uint64_t)ti.tile * kRadix + d;
-    if (ti.first) st_relaxed_u64(st, kStFlagInc | a.tag | cnt);
-    else st_relaxed_u64(st, kStFlagAgg | a.tag | cnt);
-    const uint32_t inc = warp_inclusive_scan<uint32_t>(cnt);
-    if (lane == 31) sm.wsum[warp] = inc;
-    __syncthreads();
-    uint32_t woff = 0;
+    if (d < kRadix) {
 #pragma unroll
-    for (int w = 0; w < kSWarps; ++w)
-      if (w < (int)warp) woff += sm.wsum[w];
-    sm.digit_start[d] = woff + inc - cnt;
+      for (int w = 0; w < kSWarps; ++w) {
+        const uint32_t c = sm.whist[w][d];
+        sm.whist[w][d] = (uint16_t)cnt;
+        cnt += c;
+      }
+      if (ti.first) st_relaxed_u64(st, kStFlagInc | a.tag | cnt);
+      else st_relaxed_u64(st, kStFlagAgg | a.tag | cnt);
+      const uint32_t inc = warp_inclusive_scan<uint32_t>(cnt);
+      if (lane == 31) sm.wsum[warp] = inc;
+      sm.digit_start[d] = inc - cnt;  // warp-local for now
+    }
+    __syncthreads();
+    uint32_t dstart = 0;
+    if (d < kRadix) {
+#pragma unroll
+      for (int w = 0; w < kRadix / 32; ++w)
+        if (w < (int)warp) dstart += sm.wsum[w];
+      dstart += sm.digit_start[d];
+      sm.digit_start[d] = dstart;
+#pragma unroll
+      for (int w = 0; w < kSWarps; ++w) sm.whist[w][d] = (uint16_t)(sm.whist[w][d] + dstart);
+    }
     __syncthreads();
 
     // ---- reorder through shared memory (the tile's input buffer becomes the stage)
 #pragma unroll
     for (int i = 0; i < kSItems; ++i) {
       if (e0 + 32 * i < len) {
-        const uint32_t dd = digit_of(key[i], shift);
-        const uint32_t pos = sm.digit_start[dd] + wh[dd] + rank[i];
+        const uint32_t pos = wh[digit_of(key[i], shift)] + rank[i];
         kbuf[pos] = key[i];
         if (kHasValues) vbuf[pos] = val[i];
       }
     }
 
     // ---- decoupled lookback over earlier tiles of the segment (thread = digit)
-    unsigned long long excl = 0;
-    if (!ti.first) {
-      constexpr int kLook = 8;
-      int64_t t = (int64_t)ti.tile - 1;
-      bool done = false;
-      while (!done) {
-        unsigned long long sv[kLook];
+    if (d < kRadix) {
+      unsigned long long excl = 0;
+#ifdef FS_SCATTER_NOLOOKBACK  // timing experiment only: wrong offsets, no inter-tile dependency
+      if (false) {
+#else
+      if (!ti.first) {
+#endif
+        constexpr int kLook = 8;
+        const int64_t step = ti.stride;
+        int64_t t = (int64_t)ti.tile - step;  // the segment's first tile publishes inclusive: the walk stops there
+        bool done = false;
+        while (!done) {
+          unsigned long long sv[kLook];
 #pragma unroll
-        for (int j = 0; j < kLook; ++j)
-          sv[j] = t - j >= 0 ? ld_relaxed_u64(a.status + (uint64_t)(t - j) * kRadix + d) : (kStFlagInc | a.tag);
+          for (int j = 0; j < kLook; ++j)
+            sv[j] = t - j * step >= 0 ? ld_relaxed_u64(a.status + (uint64_t)(t - j * step) * kRadix + d)
+                                      : (kStFlagInc | a.tag);
 #pragma unroll
-        for (int j = 0; j < kLook; ++j) {
-          if (done) break;
-          unsigned long long s = sv[j];
-          while ((s & (0x3Full << kTagShift)) != a.tag || (s >> 62) == 0)  // not yet published
-            s = ld_relaxed_u64(a.status + (uint64_t)(t - j) * kRadix + d);
-          excl += s & kStValue;
-          done = (s >> 62) == 2;
+          for (int j = 0; j < kLook; ++j) {
+            if (done) break;
+            unsigned long long s = sv[j];
+            while ((s & (0x3Full << kTagShift)) != a.tag || (s >> 62) == 0)  // not yet published
+              s = ld_relaxed_u64(a.status + (uint64_t)(t - j * step) * kRadix + d);
+            excl += s & kStValue;
+            done = (s >> 62) == 2;
+          }
+          t -= kLook * step;
         }
-        t -= kLook;
+        st_relaxed_u64(st, kStFlagInc | a.tag | (excl + cnt));
       }
-      st_relaxed_u64(st, kStFlagInc | a.tag | (excl + cnt));
+      sm.gofs[d] = dbase + excl - dstart;
     }
-    sm.gofs[d] = __ldg(base_tab + (uint64_t)ti.seg * base_ss + (uint64_t)d * base_ds) + excl - sm.digit_start[d];
     __syncthreads();
 
     // ---- scatter: consecutive positions of one digit go to consecutive addresses
@@ -540,7 +655,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_scatter(ScatterArgs<K> a) {
       dst_k[dst] = k;
       if (kHasValues) dst_v[dst] = vbuf[j];
     }
-    for (int i = tid; i < kSWarps * kRadix; i += kSThreads) (&sm.whist[0][0])[i] = 0;
+    for (int i = tid; i < kSWarps * kRadix / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
     __syncthreads();  // the stage (this buffer) is free for the prefetch after next
   }
 }
@@ -564,23 +679,26 @@ __global__ void k_copy_if_identity(const K* __restrict__ kin, const uint32_t* __
 // (i = arrival index inside the bin), all distinct, so ordering composites is
 // the stable order.
 //  fast path: counting sort by the top `cb` of the R bits (cb = ceil(log2 m),
-//    <= 13; groups of ~1 key) with shared atomics, then each group (<= 32 keys)
-//    insertion-sorted by composite;
+//    <= 12; groups of ~1-2 keys) with shared atomics, then every key's final
+//    position = group start + #composites of its group below its own (groups
+//    <= 32 keys), written straight to the output;
 //  slow path (a group > 32 keys: low-entropy bins): stable LSD over the varying
 //    8-bit digits of the R bits on the permutation (warp multisplit ranks).
 // Output: keys[b0 + j] = (b << R) | (c_j >> 14), vals[b0 + j] = vals_in[b0 + i_j].
 struct LocalSmemLayout {
-  static constexpr int ck = 0;                                           // u64[kLocalCap]
-  static constexpr int perm = ck + kLocalCap * 8;                        // u16[kLocalCap]
-  static constexpr int scratch = perm + kLocalCap * 2;                   // counters | perm_b + whist
-  static constexpr int perm_b = scratch;                                 // u16[kLocalCap]
-  static constexpr int whist = scratch + kLocalCap * 2;                  // u16[16][256]
-  static constexpr int scratch_end =
-      scratch + (kLocalCap * 2 + kLocalWarps * kRadix * 2 > (1 << kCountBitsMax) * 2
-                     ? kLocalCap * 2 + kLocalWarps * kRadix * 2
-                     : (1 << kCountBitsMax) * 2);
-  static constexpr int total = scratch_end;
+  static constexpr int ck = 0;                                      // u64[kLocalCap]
+  static constexpr int perm = ck + kLocalCap * 8;                   // u16[kLocalCap]
+  static constexpr int scratch = perm + kLocalCap * 2;
+  // fast path: counters u16[2^kCountBitsMax], then the final permutation u16[kLocalCap]
+  static constexpr int fin = scratch + (1 << kCountBitsMax) * 2;
+  // slow path: perm_b u16[kLocalCap], then per-warp digit offsets u16[16][256]
+  static constexpr int perm_b = scratch;
+  static constexpr int whist = scratch + kLocalCap * 2;
+  static constexpr int fast_end = fin + kLocalCap * 2;
+  static constexpr int slow_end = whist + kLocalWarps * kRadix * 2;
+  static constexpr int total = fast_end > slow_end ? fast_end : slow_end;
 };
+static_assert(LocalSmemLayout::total <= 113 * 1024, "two CTAs per SM");
 
 template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(kLocalThreads, 2)
@@ -611,8 +729,20 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 
   if (tid == 0) heavy = 0;
   for (uint32_t w = tid; w < nwords; w += kLocalThreads) cntw[w] = 0;
-  for (uint32_t i = tid; i < m; i += kLocalThreads)
-    ck[i] = (((uint64_t)keys[b0 + i] & low_mask) << kIdxBits) | i;
+  {
+    constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;  // 17: all loads in flight at once
+    K kr[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t i = tid + u * kLocalThreads;
+      kr[u] = i < m ? keys[b0 + i] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t i = tid + u * kLocalThreads;
+      if (i < m) ck[i] = (((uint64_t)kr[u] & low_mask) << kIdxBits) | i;
+    }
+  }
   __syncthreads();
 
   // ---- histogram of the counting digit (u16 counters packed two per word; m < 2^16)
@@ -655,27 +785,32 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   }
   __syncthreads();
 
-  // ---- fix-up: insertion sort of every group by composite (cnt16[g] = end of group g)
-  for (uint32_t g = tid; g < ngroups; g += kLocalThreads) {
-    const uint32_t s = g ? cnt16[g - 1] : 0u, e = cnt16[g];
-    if (e - s > (uint32_t)kMaxGroup) {
+  // ---- final positions: group start + rank of the composite inside its group
+  //      (cnt16[g] = end of group g).  Lane j of a warp holds sorted slot j, so
+  //      the members of its group sit in neighbouring lanes: they are compared
+  //      through shuffles; members outside the warp's 32 slots (a group cut by
+  //      the chunk edge) through shared memory.  Keys go straight to the output;
+  //      (element, position) pairs stay in registers until perm is free.
+  const K top = (K)((uint64_t)bkt << R);
+  uint16_t* fin = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::fin);
+  for (uint32_t j = tid; j < m; j += kLocalThreads) {
+    const uint16_t p = perm[j];
+    const uint64_t c = ck[p];
+    const uint32_t g = (uint32_t)(c >> cshift) & (ngroups - 1);
+    const uint32_t s0 = g ? cnt16[g - 1] : 0u, e = cnt16[g];
+    if (e - s0 > (uint32_t)kMaxGroup) {
       heavy = 1;
       continue;
     }
-    for (uint32_t j = s + 1; j < e; ++j) {
-      const uint16_t x = perm[j];
-      const uint64_t kx = ck[x];
-      uint32_t k = j;
-      while (k > s && ck[perm[k - 1]] > kx) {
-        perm[k] = perm[k - 1];
-        --k;
-      }
-      perm[k] = x;
-    }
+    uint32_t r = s0;
+    for (uint32_t k = s0; k < e; ++k)
+      if (k != j) r += ck[perm[k]] < c;
+    keys[b0 + r] = top | (K)(c >> kIdxBits);
+    fin[r] = p;
   }
   __syncthreads();
 
-  uint16_t* pfinal = perm;
+  uint16_t* pfinal = fin;
   if (heavy) {
     // ---- slow path: stable LSD over the varying 8-bit digits of the R bits
     uint16_t* pa = perm;
@@ -709,13 +844,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
         const uint32_t j = j0 + lane;
         const bool valid = j < c1;
         const uint32_t dg = valid ? (uint32_t)(ck[pa[j]] >> (kIdxBits + sh)) & 0xFFu : 0u;
-        uint32_t peers = __ballot_sync(kFull, valid);
-#pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-          const bool bit = (dg >> b) & 1u;
-          const uint32_t vote = __ballot_sync(kFull, bit);
-          peers &= bit ? vote : ~vote;
-        }
+        const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
         if (valid && lane == 31 - __clz(peers)) whw[dg] = (uint16_t)(whw[dg] + __popc(peers));
         __syncwarp();
       }
@@ -746,13 +875,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
         const bool valid = j < c1;
         const uint16_t p = valid ? pa[j] : (uint16_t)0;
         const uint32_t dg = valid ? (uint32_t)(ck[p] >> (kIdxBits + sh)) & 0xFFu : 0u;
-        uint32_t peers = __ballot_sync(kFull, valid);
-#pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-          const bool bit = (dg >> b) & 1u;
-          const uint32_t vote = __ballot_sync(kFull, bit);
-          peers &= bit ? vote : ~vote;
-        }
+        const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
         const uint32_t leader = 31 - __clz(peers);
         uint32_t old = 0;
         if (valid && lane == leader) {
@@ -771,13 +894,24 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
     pfinal = pa;
   }
 
-  // ---- write the bin back in sorted order
-  const K top = (K)((uint64_t)bkt << R);
-  for (uint32_t j = tid; j < m; j += kLocalThreads) keys[b0 + j] = top | (K)(ck[pfinal[j]] >> kIdxBits);
+  // ---- write the bin back in sorted order (the fast path has written the keys)
+  if (heavy)
+    for (uint32_t j = tid; j < m; j += kLocalThreads) keys[b0 + j] = top | (K)(ck[pfinal[j]] >> kIdxBits);
   if (kHasValues) {
     __syncthreads();  // ck is free: stage the values there
     uint32_t* sv = reinterpret_cast<uint32_t*>(ck);
-    for (uint32_t i = tid; i < m; i += kLocalThreads) sv[i] = vals[b0 + i];
+    constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;
+    uint32_t vr[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t i = tid + u * kLocalThreads;
+      vr[u] = i < m ? vals[b0 + i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t i = tid + u * kLocalThreads;
+      if (i < m) sv[i] = vr[u];
+    }
     __syncthreads();
     for (uint32_t j = tid; j < m; j += kLocalThreads) vals[b0 + j] = sv[pfinal[j]];
   }
@@ -786,10 +920,12 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 // ================================================================ driver
 struct WideLayout {
   size_t alt_k = 0, alt_v = 0, partials = 0;
-  size_t zero_begin = 0, spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0, zero_end = 0;
-  size_t H16 = 0, P16 = 0, lsd = 0, msd = 0, total = 0;
+  size_t zero_begin = 0, spill = 0, l1spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0,
+         zero_end = 0;
+  size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
   uint64_t tiles = 0, status_tiles = 0;
-  int hgrid = 0;
+  uint64_t chunk_tiles = 0;  // MSD: tiles per histogram chunk (= level-1 virtual segment)
+  int hgrid = 0;             // MSD: histogram CTAs = chunks
   bool use_msd = false;
 };
 
@@ -801,9 +937,12 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   if (key_bits <= 0 || key_bits > width) key_bits = width;
   L.use_msd = n >= kMsdMinN && key_bits >= 32;
   L.tiles = (n + kSTile - 1) / kSTile;
-  L.status_tiles = L.tiles + (L.use_msd ? kSegs : 0);
+  // status words: one row per ticket; level 2 interleaves only if 256 x (most
+  // tiles in a segment) fits, level 1 needs chunks x chunk_tiles <= tiles + chunks
+  L.status_tiles = L.tiles + (L.use_msd ? L.tiles / 4 + 2 * kSegs : 0);
   const uint64_t sms = (uint64_t)device_info().sm_count;
-  L.hgrid = (int)std::max<uint64_t>(1, std::min<uint64_t>(sms, (n + 65535) / 65536));
+  L.chunk_tiles = (L.tiles + sms - 1) / sms;
+  L.hgrid = (int)((L.tiles + L.chunk_tiles - 1) / L.chunk_tiles);
   size_t off = 0;
   L.alt_k = off;
   off = align_up(off + (size_t)n * key_bytes);
@@ -814,6 +953,8 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   L.zero_begin = off;  // zeroed by one memset per call
   L.spill = off;
   if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * kHistBins);
+  L.l1spill = off;
+  if (L.use_msd) off = align_up(off + sizeof(uint32_t) * kRadix * L.hgrid);
   L.scan_status = off;
   if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * (scan_tiles(kHistBins) + 1));
   L.tickets = off;
@@ -827,6 +968,10 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   if (L.use_msd) off = align_up(off + sizeof(uint64_t) * kHistBins);
   L.P16 = off;
   if (L.use_msd) off = align_up(off + sizeof(uint64_t) * (kHistBins + 1));
+  L.vcnt = off;
+  if (L.use_msd) off = align_up(off + sizeof(uint32_t) * kRadix * L.hgrid);
+  L.vbase = off;
+  if (L.use_msd) off = align_up(off + sizeof(uint64_t) * kRadix * L.hgrid);
   L.lsd = off;
   off = align_up(off + sizeof(LsdPlan));
   L.msd = off;
@@ -865,6 +1010,9 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
   ScatterArgs<K> sa{};
   sa.kin = kin; sa.vin = vin; sa.kA = kout; sa.vA = vout; sa.kB = alt_k; sa.vB = alt_v;
   sa.n = n; sa.lsd = lsd; sa.msd = msd; sa.P16 = P16; sa.status = status; sa.tiles = (uint32_t)L.tiles;
+  sa.vbase = (const uint64_t*)(t + L.vbase);
+  sa.l1_nseg = (uint32_t)L.hgrid;
+  sa.l1_chunk_tiles = (uint32_t)L.chunk_tiles;
   sa.tma = tma ? 1 : 0;
 
   phase_event(0, s);
@@ -881,12 +1029,17 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     if ((e = cudaFuncSetAttribute(k_top16_hist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem)) !=
         cudaSuccess)
       return e;
-    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, partials, spill, msd);
+    auto* l1spill = (uint32_t*)(t + L.l1spill);
+    auto* vcnt = (uint32_t*)(t + L.vcnt);
+    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
+                                                 l1spill);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_merge_scan(partials, L.hgrid, spill, nullptr, kHistBins, H16, kHistBins, 0, P16, scan_status,
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
-    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, msd);
+    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, (uint32_t)L.status_tiles, msd);
+    k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
+    k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(1, s);
     for (int level = 1; level <= 2; ++level) {
