@@ -53,6 +53,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_sort_bin.restype = i32
         L.oracle_reconstruct_all.argtypes = [vp, vp, vp, i32, i32, i32, vp]
         L.oracle_reconstruct_all.restype = None
+        L.oracle_trie_pack.argtypes = [vp, i32, u64, i32, vp, vp, vp, u64]
+        L.oracle_trie_pack.restype = ctypes.c_int64
         L.oracle_counter_width.argtypes = [i32, u64, i32]
         L.oracle_counter_width.restype = i32
         L.oracle_alg5_sort.argtypes = [vp, u64, i32, i32, vp, vp]
@@ -170,6 +172,20 @@ def reconstruct_all(E, I, C, p, l_n, l_b) -> np.ndarray:
     K = np.empty(e.size, dtype=np.uint64)
     lib().oracle_reconstruct_all(_p(e), _p(i), _p(c), p, l_n, l_b, _p(K))
     return K
+
+
+def trie_pack(levels, p, capacity, min_width=1):
+    """Tapered bit-packed export of the dense levels -> (widths, bit_offsets, packed words)."""
+    f = _flat(levels)
+    widths = np.zeros(p + 1, dtype=np.int32)
+    offs = np.zeros(p + 2, dtype=np.uint64)
+    words = ((1 << (p + 1)) * 64 + 63) // 64 + 1
+    packed = np.zeros(words, dtype=np.uint64)
+    used = lib().oracle_trie_pack(f.ctypes.data, p, capacity, min_width, widths.ctypes.data, offs.ctypes.data,
+                                  packed.ctypes.data, words)
+    if used < 0:
+        raise ValueError("oracle_trie_pack: buffer too small")
+    return widths, offs, packed[:used].copy()
 
 
 def counter_width(level, capacity, min_width=1) -> int:

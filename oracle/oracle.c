@@ -248,6 +248,44 @@ int oracle_counter_width(int level, uint64_t capacity, int min_width) {
   return w > min_width ? w : min_width;
 }
 
+/* Tapered, bit-packed export of the dense trie levels (NEXT-3 of SURVEY.md
+ * §8(f)): level l gets width w_l = oracle_counter_width(l, capacity, min_width)
+ * (§III.D.1), promoted by 4 bits while its largest
+ * counter does not fit (SPEC.md:142 overflow policy: never wrap), capped at 64.
+ * Counter i of level l occupies stream bits [off_l + i*w_l, off_l + (i+1)*w_l),
+ * off_0 = 0, off_{l+1} = off_l + 2^l * w_l; stream bit b is bit (b mod 64) of
+ * word b / 64 (LSB first).  Returns the number of words used, or -1 if
+ * `words` is too small. */
+int64_t oracle_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int* widths,
+                         uint64_t* bit_offsets, uint64_t* packed, uint64_t words) {
+  uint64_t off = 0;
+  for (int l = 0; l <= p; ++l) {
+    uint64_t mx = 0;
+    for (uint64_t i = 0; i < ((uint64_t)1 << l); ++i)
+      if (level_count(levels, l, i) > mx) mx = level_count(levels, l, i);
+    int w = oracle_counter_width(l, capacity, min_width);
+    while (w < 64 && (mx >> w) != 0) w += 4;
+    if (w > 64) w = 64;
+    widths[l] = w;
+    bit_offsets[l] = off;
+    off += ((uint64_t)1 << l) * (uint64_t)w;
+  }
+  bit_offsets[p + 1] = off;
+  const uint64_t used = (off + 63) / 64;
+  if (used > words) return -1;
+  memset(packed, 0, sizeof(uint64_t) * used);
+  for (int l = 0; l <= p; ++l) {
+    for (uint64_t i = 0; i < ((uint64_t)1 << l); ++i) {
+      const uint64_t x = level_count(levels, l, i);
+      for (int b = 0; b < widths[l]; ++b) {  /* one bit at a time: obviously correct */
+        const uint64_t pos = bit_offsets[l] + i * (uint64_t)widths[l] + (uint64_t)b;
+        packed[pos / 64] |= ((x >> b) & 1u) << (pos % 64);
+      }
+    }
+  }
+  return (int64_t)used;
+}
+
 /* ---------------------------------------------------------- LSD pairs / keys */
 
 int oracle_sort_pairs_u64_u32(const uint64_t* kin, const uint32_t* vin, uint64_t n, int key_bits,

@@ -74,6 +74,14 @@ int oracle_alg5_sort(const uint64_t* keys, uint64_t n, int p, int l_b, uint64_t*
  * (§III.D.1, 197 §III.F.1; ledger 11). */
 int oracle_counter_width(int level, uint64_t capacity, int min_width);
 
+/* Tapered, bit-packed export of the dense levels (NEXT-3):
+ * w_l = counter_width(l, capacity, min_width) promoted by +4 until the level's
+ * largest counter fits (<= 64); counter i of level l at stream bits
+ * [off_l + i w_l, off_l + (i+1) w_l), LSB-first in u64 words.  widths: p+1,
+ * bit_offsets: p+2.  Returns words used, -1 if `words` is too small. */
+int64_t oracle_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int* widths,
+                         uint64_t* bit_offsets, uint64_t* packed, uint64_t words);
+
 /* Stable LSD radix sort ("histogram, prefix sum and stable scatter phases",
  * PAPER.md:52) with 16-bit digits over the low key_bits bits.
  * vals may be NULL (keys-only).  Each pass: count, exclusive scan, stable

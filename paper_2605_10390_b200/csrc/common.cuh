@@ -17,9 +17,20 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 FS_DEVINL uint4 ld_stream_v4(const uint4* p) { return __ldcs(p); }
 
 // 128-bit streaming store (written once, not re-read by this kernel).
+#ifndef FS_STORE_FLAVOR  // scripts/microbench: 0 .cs, 1 plain (write-back), 2 .L1::no_allocate
+#define FS_STORE_FLAVOR 0
+#endif
 FS_DEVINL void st_stream_v4(uint4* p, uint4 v) {
+#if FS_STORE_FLAVOR == 1
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+#elif FS_STORE_FLAVOR == 2
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+#else
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+#endif
 }
 
 // 64-bit status words of the decoupled lookbacks.  A status word carries its own

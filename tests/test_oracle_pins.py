@@ -267,3 +267,41 @@ def test_send_counts_bruteforce(G):
     want = _send_counts_bruteforce(shards, G)
     for g in range(G):
         np.testing.assert_array_equal(oracle.send_counts(C_all, g), want[g])
+
+
+# ------------------------------------------------------------- NEXT-3: tapered bit-packed trie export
+def test_golden_trie_pack_hand_example():
+    g = GOLD["trie_pack_1_3_3"]
+    lv = oracle.trie_levels(np.array(g["keys"]), g["p"])
+    w, off, words = oracle.trie_pack(lv, g["p"], g["capacity"], g["min_width"])
+    assert w.tolist() == g["widths"]
+    assert off.tolist() == g["bit_offsets"]
+    assert words.tolist() == g["words"]
+
+
+def _unpack(words, off, w, p):
+    """Independent reader: Python big-integer bit slicing of the packed stream."""
+    big = 0
+    for i, x in enumerate(words.tolist()):
+        big |= int(x) << (64 * i)
+    out = []
+    for l in range(p + 1):
+        out.append(np.array([(big >> (int(off[l]) + i * int(w[l]))) & ((1 << int(w[l])) - 1)
+                             for i in range(1 << l)], dtype=np.uint64))
+    return out
+
+
+@pytest.mark.parametrize("dist,n,p", [("uniform", 5000, 10), ("const", 777, 8), ("zipf", 20000, 12)])
+def test_trie_pack_roundtrip_and_widths(dist, n, p):
+    keys = datagen.gen_u16(dist, n, seed=3).astype(np.uint64) >> np.uint64(16 - p)
+    lv = oracle.trie_levels(keys, p)
+    w, off, words = oracle.trie_pack(lv, p, n, 2)
+    back = _unpack(words, off, w, p)
+    for l in range(p + 1):
+        np.testing.assert_array_equal(back[l], lv[l])
+        need = int(lv[l].max()).bit_length()
+        base = oracle.counter_width(l, n, 2)
+        # tapered width, promoted by exactly as many +4 steps as the level's largest count requires
+        k = 0 if need <= base else -(-(need - base) // 4)
+        assert w[l] == min(64, base + 4 * k)
+        assert int(off[l + 1]) - int(off[l]) == (1 << l) * int(w[l])
