@@ -184,6 +184,60 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
                                 uint64_t batch, void* work, size_t work_bytes, fs_stream_t stream);
 
 /* ----------------------------------------------------------------------------
+ * Order-statistic service on the compressed histogram:
+ * quantiles, ranks and splitters without sorting.
+ *
+ * fs_trie_levels: the dense trie of a leaf histogram.  leaf_hist: 2^p u64
+ * counts (e.g. fs_histogram_u16's output, p = key_bits); levels: receives
+ * fs_trie_levels_count(p) = 2^(p+1) - 1 u64, level l (0 = root) at offset
+ * 2^l - 1, node i of level l = #keys whose top l bits (MSB-first, ledger 1)
+ * equal i = the sum of its two children (Alg. 1 PAPER.md:113-139 with the
+ * SIBLING SUM of SPEC.md:127; dense computable-pointer layout, Alg. 4
+ * PAPER.md:196-215).  p in 1..24; the buffers must not overlap.
+ * ------------------------------------------------------------------------- */
+size_t fs_trie_levels_count(int p);
+fs_status fs_trie_levels(const uint64_t* leaf_hist, int p, uint64_t* levels, fs_stream_t stream);
+
+/* fs_trie_pack: tapered, bit-packed export of the levels (counter-width
+ * compression, §III.D.1): level l gets
+ * w_l = max(min_width, ceil(log2(capacity + 1)) - l), promoted by +4 bits while
+ * its largest counter does not fit, capped at 64 (never wrap, SPEC.md:142;
+ * ledger 12).  Counter i of level l occupies stream bits
+ * [off_l + i w_l, off_l + (i+1) w_l), off_0 = 0, off_{l+1} = off_l + 2^l w_l;
+ * stream bit b is bit (b mod 64) of packed[b / 64].  Device outputs: widths
+ * (p+1 int32), bit_offsets (p+2 u64), packed (packed_words u64, zeroed and
+ * written).  capacity should be >= the total count (the root); then
+ * fs_trie_pack_words(p, capacity) words always suffice.  If the stream does not
+ * fit in packed_words, widths[0] is set to -1 and packed is left zeroed.
+ * temp: fs_trie_pack_temp_bytes(p) device bytes.  min_width in 1..64. */
+size_t fs_trie_pack_words(int p, uint64_t capacity);
+size_t fs_trie_pack_temp_bytes(int p);
+fs_status fs_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int32_t* widths,
+                       uint64_t* bit_offsets, uint64_t* packed, uint64_t packed_words, void* temp,
+                       size_t temp_bytes, fs_stream_t stream);
+
+/* Batched queries on a packed trie (as written by fs_trie_pack), q queries, one
+ * thread each, every array on the device:
+ *   fs_get_item:  items[k] = the key at ascending sorted rank ranks[k] (0-based),
+ *                 or default_value if ranks[k] >= total — Alg. 2 GetItem
+ *                  as order-statistic descent on the LEFT
+ *                 child's count (ledger 4), the key rebuilt from the path (ledger 5);
+ *   fs_get_index: indices[k] = #keys < values[k] — Alg. 3 GetIndex
+ *                 (ledger 6); values[k] must be < 2^p (only
+ *                 the low p bits are walked otherwise). */
+fs_status fs_get_item(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
+                      const uint64_t* ranks, uint64_t q, uint64_t default_value, uint64_t* items,
+                      fs_stream_t stream);
+fs_status fs_get_index(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
+                       const uint64_t* values, uint64_t q, uint64_t* indices, fs_stream_t stream);
+
+/* fs_hist_merge_u64: out[i] = a[i] + b[i] for i < count — the merge of two
+ * histograms (or two dense tries) "aggregated into a single ... tree"
+ * (§III.A.1).  out may alias a or b. */
+fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t count,
+                            fs_stream_t stream);
+
+/* ----------------------------------------------------------------------------
  * Phase instrumentation (measurement).  events: array of
  * `count` cudaEvent_t handles (created by the caller), or NULL to disable.
  * While set, the sort calls made on THIS thread record events[i] on their

@@ -21,6 +21,7 @@ from ._lib import FractalSortError, check, lib
 __all__ = [
     "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
+    "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
 ]
 
 _TEMP_ALIGN = 256
@@ -189,3 +190,70 @@ def sort_keys_u16_host(keys_host: torch.Tensor, out_host: torch.Tensor | None = 
         if synchronize:
             torch.cuda.current_stream(dev).synchronize()
     return out_host
+
+
+# ---------------------------------------------------------------- order statistics (NEXT-3)
+def trie_levels(leaf_hist: torch.Tensor, p: int) -> torch.Tensor:
+    """Dense trie levels (2^(p+1) - 1 int64, level l at offset 2^l - 1) from a 2^p leaf histogram."""
+    dev = _require_cuda(leaf_hist)
+    if leaf_hist.dtype not in (torch.int64, torch.uint64) or leaf_hist.numel() != (1 << p):
+        raise ValueError("leaf_hist must hold 2^p int64/uint64 counters")
+    L = lib()
+    levels = torch.empty(L.fs_trie_levels_count(p), dtype=leaf_hist.dtype, device=dev)
+    with torch.cuda.device(dev):
+        check(L.fs_trie_levels(leaf_hist.data_ptr(), p, levels.data_ptr(), _stream(dev)), "fs_trie_levels")
+    return levels
+
+
+class PackedTrie:
+    """A tapered bit-packed trie on the device (fs_trie_pack output)."""
+
+    def __init__(self, p: int, widths: torch.Tensor, bit_offsets: torch.Tensor, packed: torch.Tensor):
+        self.p, self.widths, self.bit_offsets, self.packed = p, widths, bit_offsets, packed
+
+
+def trie_pack(levels: torch.Tensor, p: int, capacity: int, min_width: int = 1) -> PackedTrie:
+    dev = _require_cuda(levels)
+    L = lib()
+    words = L.fs_trie_pack_words(p, capacity)
+    widths = torch.empty(p + 1, dtype=torch.int32, device=dev)
+    offs = torch.empty(p + 2, dtype=torch.int64, device=dev)
+    packed = torch.empty(words, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_trie_pack_temp_bytes(p), dev)
+        check(L.fs_trie_pack(levels.data_ptr(), p, capacity, min_width, widths.data_ptr(), offs.data_ptr(),
+                             packed.data_ptr(), words, temp.data_ptr(), temp.numel(), _stream(dev)), "fs_trie_pack")
+    return PackedTrie(p, widths, offs, packed)
+
+
+def get_item(t: PackedTrie, ranks: torch.Tensor, default: int = 0) -> torch.Tensor:
+    """Keys at ascending sorted ranks (Alg. 2), default where rank >= total (fs_get_item)."""
+    dev = _require_cuda(ranks, t.packed)
+    items = torch.empty(ranks.numel(), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_get_item(t.widths.data_ptr(), t.bit_offsets.data_ptr(), t.packed.data_ptr(), t.p,
+                                ranks.data_ptr(), ranks.numel(), default, items.data_ptr(), _stream(dev)),
+              "fs_get_item")
+    return items
+
+
+def get_index(t: PackedTrie, values: torch.Tensor) -> torch.Tensor:
+    """#keys < value for each value (Alg. 3, fs_get_index)."""
+    dev = _require_cuda(values, t.packed)
+    idx = torch.empty(values.numel(), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_get_index(t.widths.data_ptr(), t.bit_offsets.data_ptr(), t.packed.data_ptr(), t.p,
+                                 values.data_ptr(), values.numel(), idx.data_ptr(), _stream(dev)), "fs_get_index")
+    return idx
+
+
+def hist_merge(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = a + b, counter by counter (fs_hist_merge_u64)."""
+    dev = _require_cuda(a, b)
+    if a.numel() != b.numel():
+        raise ValueError("a and b must have the same number of counters")
+    out = torch.empty_like(a) if out is None else out
+    with torch.cuda.device(dev):
+        check(lib().fs_hist_merge_u64(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _stream(dev)),
+              "fs_hist_merge_u64")
+    return out

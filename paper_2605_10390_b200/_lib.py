@@ -36,6 +36,14 @@ SIGNATURES = {
     "fs_sort_keys_u16_host_work_bytes": (_sz, [_u64, _u64]),
     "fs_sort_keys_u16_host": (_i32, [_vp, _vp, _u64, _u64, _vp, _sz, _vp]),
     "fs_set_phase_events": (_i32, [_vp, _i32]),
+    "fs_trie_levels_count": (_sz, [_i32]),
+    "fs_trie_levels": (_i32, [_vp, _i32, _vp, _vp]),
+    "fs_trie_pack_words": (_sz, [_i32, _u64]),
+    "fs_trie_pack_temp_bytes": (_sz, [_i32]),
+    "fs_trie_pack": (_i32, [_vp, _i32, _u64, _i32, _vp, _vp, _vp, _u64, _vp, _sz, _vp]),
+    "fs_get_item": (_i32, [_vp, _vp, _vp, _i32, _vp, _u64, _u64, _vp, _vp]),
+    "fs_get_index": (_i32, [_vp, _vp, _vp, _i32, _vp, _u64, _vp, _vp]),
+    "fs_hist_merge_u64": (_i32, [_vp, _vp, _vp, _u64, _vp]),
 }
 
 _lib = None

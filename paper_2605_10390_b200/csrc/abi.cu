@@ -264,6 +264,96 @@ fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins,
   return finish(s, "fs_send_counts");
 }
 
+// ------------------------------------------------------------ NEXT-3: order statistics
+size_t fs_trie_levels_count(int p) { return (p < 1 || p > 24) ? 0 : (((size_t)2 << p) - 1); }
+
+fs_status fs_trie_levels(const uint64_t* leaf_hist, int p, uint64_t* levels, fs_stream_t stream) {
+  clear_error();
+  if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
+  if (!leaf_hist || !levels) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (overlaps(leaf_hist, ((size_t)1 << p) * 8, levels, fs_trie_levels_count(p) * 8))
+    return fail(FS_ERR_INVALID_ARGUMENT, "leaf_hist and levels overlap");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_trie_levels(leaf_hist, p, levels, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_trie_levels");
+  return finish(s, "fs_trie_levels");
+}
+
+static int bitlen_u64(uint64_t x) {
+  int b = 0;
+  while (b < 64 && (x >> b) != 0) ++b;
+  return b;
+}
+
+size_t fs_trie_pack_words(int p, uint64_t capacity) {
+  if (p < 1 || p > 24) return 0;
+  // widths never exceed bitlen(capacity) + 3 when every count <= capacity
+  int full = bitlen_u64(capacity);
+  uint64_t bits = 0;
+  for (int l = 0; l <= p; ++l) {
+    int w = full + 3;
+    if (w > 64) w = 64;
+    bits += ((uint64_t)1 << l) * (uint64_t)w;
+  }
+  return (size_t)((bits + 63) / 64);
+}
+
+size_t fs_trie_pack_temp_bytes(int p) { return (p < 1 || p > 24) ? 0 : align_up(sizeof(uint64_t) * (p + 1)); }
+
+fs_status fs_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int32_t* widths,
+                       uint64_t* bit_offsets, uint64_t* packed, uint64_t packed_words, void* temp,
+                       size_t temp_bytes, fs_stream_t stream) {
+  clear_error();
+  if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
+  if (min_width < 1 || min_width > 64) return fail(FS_ERR_INVALID_ARGUMENT, "min_width %d not in 1..64", min_width);
+  if (!levels || !widths || !bit_offsets || !packed || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (temp_bytes < fs_trie_pack_temp_bytes(p))
+    return fail(FS_ERR_INVALID_ARGUMENT, "temp_bytes %zu < required %zu", temp_bytes, fs_trie_pack_temp_bytes(p));
+  if (packed_words == 0) return fail(FS_ERR_INVALID_ARGUMENT, "packed_words is 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_trie_pack(levels, p, capacity, min_width, widths, bit_offsets, packed, packed_words,
+                                   (unsigned long long*)temp, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_trie_pack");
+  return finish(s, "fs_trie_pack");
+}
+
+fs_status fs_get_item(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
+                      const uint64_t* ranks, uint64_t q, uint64_t default_value, uint64_t* items,
+                      fs_stream_t stream) {
+  clear_error();
+  if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
+  if (q == 0) return FS_OK;
+  if (!widths || !bit_offsets || !packed || !ranks || !items) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_get_item(widths, bit_offsets, packed, p, ranks, q, default_value, items, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_get_item");
+  return finish(s, "fs_get_item");
+}
+
+fs_status fs_get_index(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
+                       const uint64_t* values, uint64_t q, uint64_t* indices, fs_stream_t stream) {
+  clear_error();
+  if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
+  if (q == 0) return FS_OK;
+  if (!widths || !bit_offsets || !packed || !values || !indices)
+    return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_get_index(widths, bit_offsets, packed, p, values, q, indices, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_get_index");
+  return finish(s, "fs_get_index");
+}
+
+fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t count,
+                            fs_stream_t stream) {
+  clear_error();
+  if (count == 0) return FS_OK;
+  if (!a || !b || !out) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_hist_merge(a, b, out, count, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_hist_merge_u64");
+  return finish(s, "fs_hist_merge_u64");
+}
+
 static fs_status wide_sort(const char* name, const void* kin, const uint32_t* vin, void* kout, uint32_t* vout,
                            uint64_t n, int key_bytes, int key_bits, void* temp, size_t temp_bytes,
                            fs_stream_t stream) {

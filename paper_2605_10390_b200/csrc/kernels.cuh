@@ -56,6 +56,19 @@ cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64
 cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                                cudaStream_t s);
 
+// ---------------------------------------------------------------- trie.cu
+// Order-statistic service (NEXT-3): dense levels, tapered bit-packed export, queries.
+cudaError_t launch_trie_levels(const uint64_t* leaves, int p, uint64_t* levels, cudaStream_t s);
+cudaError_t launch_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int32_t* widths,
+                             uint64_t* off, uint64_t* packed, uint64_t words, unsigned long long* mx,
+                             cudaStream_t s);
+cudaError_t launch_get_item(const int32_t* widths, const uint64_t* off, const uint64_t* packed, int p,
+                            const uint64_t* ranks, uint64_t q, uint64_t default_value, uint64_t* items,
+                            cudaStream_t s);
+cudaError_t launch_get_index(const int32_t* widths, const uint64_t* off, const uint64_t* packed, int p,
+                             const uint64_t* values, uint64_t q, uint64_t* indices, cudaStream_t s);
+cudaError_t launch_hist_merge(const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t count, cudaStream_t s);
+
 // ---------------------------------------------------------------- wide.cu
 // Stable sort of u32/u64 keys (+ optional u32 values): trie-binned MSD with a
 // per-bin local sort when every 16-bit bin fits shared memory (decided on the

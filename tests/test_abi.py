@@ -69,6 +69,13 @@ V = ctypes.c_void_p
     lambda L: L.fs_send_counts(V(0x1000), 2, 2, 16, V(0x8000), None),                         # g >= G
     lambda L: L.fs_histogram_u16(V(0x1000), 10, 0, None, 0, V(0x100000), 1 << 30, None),     # hist NULL
     lambda L: L.fs_sort_keys_u16_host(None, V(0x2000), 10, 0, V(0x100000), 1 << 30, None),
+    lambda L: L.fs_trie_levels(V(0x1000), 25, V(0x100000), None),                             # p > 24
+    lambda L: L.fs_trie_levels(V(0x1000), 4, V(0x1000), None),                                # overlap
+    lambda L: L.fs_trie_pack(V(0x1000), 16, 100, 0, V(0x2000), V(0x3000), V(0x4000), 100, V(0x8000), 256, None),
+    lambda L: L.fs_trie_pack(V(0x1000), 16, 100, 1, V(0x2000), V(0x3000), V(0x4000), 100, V(0x8000), 8, None),
+    lambda L: L.fs_get_item(None, V(0x3000), V(0x4000), 16, V(0x5000), 4, 0, V(0x6000), None),
+    lambda L: L.fs_get_index(V(0x2000), V(0x3000), V(0x4000), 0, V(0x5000), 4, V(0x6000), None),
+    lambda L: L.fs_hist_merge_u64(V(0x1000), None, V(0x3000), 4, None),
 ])
 def test_invalid_arguments_rejected_without_gpu(call):
     L = fs.lib()
@@ -81,6 +88,17 @@ def test_n_zero_is_ok_without_launch():
     assert L.fs_sort_keys_u16(None, None, 0, 0, None, 0, None) == _lib.FS_OK
     assert L.fs_sort_pairs_u64_u32(None, None, None, None, 0, 0, None, 0, None) == _lib.FS_OK
     assert L.fs_expand_u16(V(0x1000), 16, 7, 7, V(0x8000), None) == _lib.FS_OK
+    assert L.fs_get_item(None, None, None, 16, None, 0, 0, None, None) == _lib.FS_OK
+    assert L.fs_hist_merge_u64(None, None, None, 0, None) == _lib.FS_OK
+
+
+def test_trie_sizes():
+    L = fs.lib()
+    assert L.fs_trie_levels_count(16) == (1 << 17) - 1
+    assert L.fs_trie_levels_count(0) == 0
+    # the word bound covers widths of bitlen(capacity) + 3 on every level
+    assert L.fs_trie_pack_words(16, (1 << 28)) * 64 >= ((1 << 17) - 1) * 32
+    assert L.fs_trie_pack_temp_bytes(16) >= 17 * 8
 
 
 def test_temp_sizes_are_monotone_and_aligned():
