@@ -165,6 +165,25 @@ fs_status fs_expand_u16(const uint64_t* prefix, uint64_t nbins, uint64_t out_beg
 fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                          fs_stream_t stream);
 
+/* fs_expand_to_peers_u16: the fused exchange of the multi-GPU keys-only sort
+ * (SURVEY.md §8(f) NEXT-2): rank g writes each of its own keys straight to its
+ * final global sorted position, in the output buffer of the rank that owns it.
+ * hist_all: G x nbins u64 on the device (row r = rank r's histogram, as
+ * gathered).  With N = total and P = exclusive scan of sum_r C_r, rank g's keys
+ * of value v go to global positions [P[v] + S_<g[v], P[v] + S_<=g[v]) (lower
+ * rank first), and rank d owns positions [floor(dN/G),
+ * floor((d+1)N/G)) (ledger 23): dest[d] (a HOST array of G device pointers,
+ * each dest[d] a device — normally peer-mapped via CUDA IPC — buffer of at
+ * least floor((d+1)N/G) - floor(dN/G) u16) receives them at offset
+ * position - floor(dN/G).  After every rank's call has completed (synchronise,
+ * then a barrier across ranks), each rank's buffer holds its slice of the sorted
+ * output: Alg. 5 count-expansion done by the producers.
+ * temp: fs_expand_to_peers_u16_temp_bytes(nbins, G) device bytes.  The call
+ * returns when the work is enqueued (dest is copied to the device in order). */
+size_t fs_expand_to_peers_u16_temp_bytes(uint64_t nbins, int G);
+fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest,
+                                 void* temp, size_t temp_bytes, fs_stream_t stream);
+
 /* ----------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use, and the out-of-core path of Batch
  * Size Selection / Batch Counter Update): sorts n u16 keys

@@ -21,7 +21,7 @@ from ._lib import FractalSortError, check, lib
 __all__ = [
     "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
-    "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
+    "expand_to_peers_u16", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
 ]
 
 _TEMP_ALIGN = 256
@@ -159,6 +159,22 @@ def send_counts(hist_all: torch.Tensor, g: int) -> torch.Tensor:
         check(lib().fs_send_counts(hist_all.data_ptr(), G, g, nb, send.data_ptr(), _stream(dev)),
               "fs_send_counts")
     return send
+
+
+def expand_to_peers_u16(hist_all: torch.Tensor, g: int, dest: list) -> None:
+    """Rank g writes its keys to their final sorted positions in dest[d] (the
+    buffer of the rank owning them; peer-mapped tensors), fs_expand_to_peers_u16."""
+    import ctypes
+    dev = _require_cuda(hist_all)
+    G, nb = hist_all.shape
+    if len(dest) != G:
+        raise ValueError("dest must hold one buffer per rank")
+    ptrs = (ctypes.c_void_p * G)(*[t.data_ptr() for t in dest])
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_expand_to_peers_u16_temp_bytes(nb, G), dev)
+        check(L.fs_expand_to_peers_u16(hist_all.data_ptr(), G, g, nb, ptrs, temp.data_ptr(), temp.numel(),
+                                       _stream(dev)), "fs_expand_to_peers_u16")
 
 
 def sort_keys_u16_host_work_bytes(n: int, batch: int = 0) -> int:

@@ -264,6 +264,28 @@ fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins,
   return finish(s, "fs_send_counts");
 }
 
+// ------------------------------------------------------------ NEXT-2: fused expand-to-peer
+size_t fs_expand_to_peers_u16_temp_bytes(uint64_t nbins, int G) {
+  return (nbins == 0 || nbins > 65536 || G < 1 || G > 1024) ? 0 : expand_to_peers_temp_bytes(nbins, G);
+}
+
+fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest,
+                                 void* temp, size_t temp_bytes, fs_stream_t stream) {
+  clear_error();
+  if (G < 1 || G > 1024 || g < 0 || g >= G) return fail(FS_ERR_INVALID_ARGUMENT, "bad G=%d g=%d", G, g);
+  if (nbins == 0 || nbins > 65536) return fail(FS_ERR_INVALID_ARGUMENT, "nbins not in 1..65536");
+  if (!hist_all || !dest || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  for (int d = 0; d < G; ++d)
+    if (!dest[d]) return fail(FS_ERR_INVALID_ARGUMENT, "dest[%d] is NULL", d);
+  if ((uintptr_t)temp & 255) return fail(FS_ERR_INVALID_ARGUMENT, "temp not 256-byte aligned");
+  const size_t need = expand_to_peers_temp_bytes(nbins, G);
+  if (temp_bytes < need) return fail(FS_ERR_INVALID_ARGUMENT, "temp_bytes %zu < required %zu", temp_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_expand_to_peers(hist_all, G, g, nbins, dest, temp, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_expand_to_peers_u16");
+  return finish(s, "fs_expand_to_peers_u16");
+}
+
 // ------------------------------------------------------------ NEXT-3: order statistics
 size_t fs_trie_levels_count(int p) { return (p < 1 || p > 24) ? 0 : (((size_t)2 << p) - 1); }
 

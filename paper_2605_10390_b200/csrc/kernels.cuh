@@ -56,6 +56,11 @@ cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64
 cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                                cudaStream_t s);
 
+// ---------------------------------------------------------------- peer.cu
+size_t expand_to_peers_temp_bytes(uint64_t nbins, int G);
+cudaError_t launch_expand_to_peers(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest_host,
+                                   void* temp, cudaStream_t s);
+
 // ---------------------------------------------------------------- trie.cu
 // Order-statistic service (NEXT-3): dense levels, tapered bit-packed export, queries.
 cudaError_t launch_trie_levels(const uint64_t* leaves, int p, uint64_t* levels, cudaStream_t s);

@@ -15,6 +15,12 @@ mode "A" (payload exchange by key range, the literal c4 reading): local sort of
     the shard, all_gather of the histograms, exact send counts (fs_send_counts:
     lower rank first for equal keys), all_to_all_single of the key
     bytes, and a local sort of what arrived.
+mode "P" (fused expand-to-peer): all_gather of the
+    histograms, then every rank writes each of its own keys straight to its
+    final sorted position in the owning rank's output buffer, mapped into its
+    address space with CUDA IPC (NVLink / NVSwitch peer stores,
+    fs_expand_to_peers_u16); a barrier ends the exchange.  The payload crosses
+    NVLink once and no rank sorts anything.
 
 ``ops`` supplies the local steps.  The default, CudaOps, calls the library's
 kernels through the binding; the gloo tests on CPU inject their own stand-ins
@@ -49,6 +55,34 @@ class CudaOps:
         from . import send_counts
         return send_counts(hist_all, g)             # int64[G]
 
+    def expand_to_peers(self, hist_all, g, dest):
+        from . import expand_to_peers_u16
+        expand_to_peers_u16(hist_all, g, dest)
+
+    def synchronize(self, device):
+        torch.cuda.synchronize(device)
+
+
+class PeerBuffers:
+    """Every rank's output buffer, mapped into every rank (CUDA IPC through
+    torch's tensor sharing; peer access over NVLink is enabled by the mapping).
+    Buffers hold ceil(N / G) keys (every rank's range fits) and are reallocated,
+    collectively, only when a larger N arrives."""
+
+    def __init__(self, device, group=None):
+        self.device, self.group, self.capacity, self.views = device, group, 0, None
+
+    def buffers(self, per_rank: int):
+        if per_rank > self.capacity:
+            from torch.multiprocessing.reductions import reduce_tensor
+            world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+            own = torch.empty(max(per_rank, 1), dtype=torch.uint16, device=self.device)
+            handles = [None] * world
+            dist.all_gather_object(handles, reduce_tensor(own) if world > 1 else None, group=self.group)
+            self.views = [own if r == rank else handles[r][0](*handles[r][1]) for r in range(world)]
+            self.capacity = per_rank
+        return self.views
+
 
 def output_range(rank: int, world: int, n_total: int):
     """Rank's global sorted positions [floor(r N / G), floor((r+1) N / G))."""
@@ -61,9 +95,11 @@ def _total_keys(n_local: int, device, group) -> int:
     return int(t.item())
 
 
-def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None):
+def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, peers=None):
     """Sort the union of all ranks' shards; returns (this rank's slice of the sorted
-    output, (begin, end) global positions of that slice)."""
+    output, (begin, end) global positions of that slice).  mode "P" writes into
+    ``peers.buffers(...)`` (a PeerBuffers by default; pass one to reuse the
+    mappings across calls) and returns a view of this rank's buffer."""
     if shard.dtype != torch.uint16 or shard.dim() != 1:
         raise TypeError("shard must be a 1-D uint16 tensor")
     ops = ops or CudaOps()
@@ -98,4 +134,18 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None):
                                input_split_sizes=[2 * c for c in send_list], group=group)
         out = ops.sort_keys(recv_buf) if recv_buf.numel() else recv_buf
         return out, (begin, end)
+    if mode == "P":
+        hist = ops.histogram_u16(shard)
+        gathered = [torch.empty_like(hist) for _ in range(world)]
+        dist.all_gather(gathered, hist, group=group)
+        hist_all = torch.stack(gathered)                       # G x 65536
+        n_total = int(hist_all.sum().item())
+        begin, end = output_range(rank, world, n_total)
+        if peers is None:
+            peers = PeerBuffers(dev, group)
+        dest = peers.buffers(-(-n_total // world))
+        ops.expand_to_peers(hist_all, rank, dest)
+        ops.synchronize(dev)
+        dist.barrier(group=group)                              # every producer has finished writing
+        return dest[rank][:end - begin], (begin, end)
     raise ValueError(f"unknown mode {mode!r}")

@@ -44,6 +44,40 @@ class OracleOps:
         import oracle
         return torch.from_numpy(oracle.send_counts(hist_all.numpy().astype(np.uint64), g).astype(np.int64))
 
+    def expand_to_peers(self, hist_all, g, dest):
+        """Rank g's keys to their global positions (P[v] + S_<g[v] + local offset) in
+        the owning rank's buffer -- the definition, with the oracle's scans."""
+        import oracle
+        C = hist_all.numpy().astype(np.uint64)
+        G = C.shape[0]
+        P = oracle.exclusive_scan(C.sum(axis=0))
+        S = C[:g].sum(axis=0) if g else np.zeros(C.shape[1], dtype=np.uint64)
+        Pg = oracle.exclusive_scan(C[g])
+        vals = oracle.reconstruct_counts_u16(C[g], 0, int(Pg[-1]))  # rank g's keys in sorted order
+        v = vals.astype(np.int64)
+        j = np.arange(vals.size, dtype=np.uint64)
+        pos = P[v] + S[v] + j - Pg[v]
+        N = int(P[-1])
+        begins = np.array([(N * d) // G for d in range(G + 1)], dtype=np.uint64)
+        owner = np.searchsorted(begins, pos, side="right") - 1
+        for d in range(G):
+            sel = owner == d
+            dest[d].numpy()[(pos[sel] - begins[d]).astype(np.int64)] = vals[sel]
+
+    def synchronize(self, device):
+        pass
+
+
+class SharedPeers:
+    """CPU stand-in of dist.PeerBuffers: shared-memory buffers made by the parent."""
+
+    def __init__(self, bufs):
+        self.bufs = bufs
+
+    def buffers(self, per_rank):
+        assert all(b.numel() >= per_rank for b in self.bufs)
+        return self.bufs
+
 
 def free_port():
     s = socket.socket()
@@ -63,12 +97,12 @@ def shard_bounds(n_total, world, rank, uneven):
     return cuts[rank], cuts[rank + 1]
 
 
-CASES = [(mode, d, uneven) for mode in ("B", "A")
+CASES = [(mode, d, uneven) for mode in ("B", "A", "P")
          for d, uneven in (("uniform", False), ("zipf", True), ("const", False), ("sortedswap", True))]
 N_TOTAL = 50_003
 
 
-def worker(rank, world, port, outdir):
+def worker(rank, world, port, outdir, peer_bufs):
     sys.path.insert(0, ROOT)
     import datagen
     from paper_2605_10390_b200 import dist as fsdist
@@ -80,7 +114,8 @@ def worker(rank, world, port, outdir):
             b, e = shard_bounds(N_TOTAL, world, rank, uneven)
             full = datagen.gen_u16(dist_name, N_TOTAL, seed=3)
             shard = torch.from_numpy(full[b:e].copy())
-            out, (ob, oe) = fsdist.sort_keys_u16(shard, mode=mode, ops=OracleOps())
+            peers = SharedPeers(peer_bufs[ci]) if mode == "P" else None
+            out, (ob, oe) = fsdist.sort_keys_u16(shard, mode=mode, ops=OracleOps(), peers=peers)
             np.save(os.path.join(outdir, f"out_{ci}_{rank}.npy"), out.numpy())
             np.save(os.path.join(outdir, f"range_{ci}_{rank}.npy"), np.array([ob, oe], dtype=np.int64))
     finally:
@@ -89,10 +124,12 @@ def worker(rank, world, port, outdir):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_distributed_sort_matches_oracle(tmp_path, world):
-    """Modes A and B, four distributions (uneven and empty shards included)."""
+    """Modes A, B and P (expand-to-peer), four distributions (uneven and empty shards included)."""
     import datagen
     import oracle
-    mp.start_processes(worker, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True,
+    cap = -(-N_TOTAL // world)
+    peer_bufs = [[torch.zeros(cap, dtype=torch.uint16).share_memory_() for _ in range(world)] for _ in CASES]
+    mp.start_processes(worker, args=(world, free_port(), str(tmp_path), peer_bufs), nprocs=world, join=True,
                        start_method="spawn")
     for ci, (mode, dist_name, uneven) in enumerate(CASES):
         outs = [np.load(tmp_path / f"out_{ci}_{r}.npy") for r in range(world)]

@@ -28,10 +28,31 @@ def nccl_group(cuda):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["B", "A"])
+@pytest.mark.parametrize("mode", ["B", "A", "P"])
 @pytest.mark.parametrize("dist_name", ["uniform", "zipf", "const"])
 def test_dist_single_rank(cuda, nccl_group, mode, dist_name):
     keys = datagen.gen_u16(dist_name, 1_000_003, seed=1)
     out, (b, e) = fsdist.sort_keys_u16(torch.from_numpy(keys).to(cuda), mode=mode)
     assert (b, e) == (0, keys.size)
     np.testing.assert_array_equal(out.cpu().numpy(), oracle.sort_u16(keys))
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("dist_name", ["uniform", "zipf", "const", "sortedswap"])
+def test_expand_to_peers_virtual_ranks(cuda, G, dist_name):
+    """fs_expand_to_peers_u16 for every rank g of a G-rank job, issued from one
+    GPU into G separate buffers (each call only writes; no call waits on
+    another): the buffers concatenate to the oracle sort of the whole input."""
+    import paper_2605_10390_b200 as fs
+    n = 2_000_003
+    keys = datagen.gen_u16(dist_name, n, seed=G)
+    cuts = [0] + sorted((n * (2 * r + 1)) // (2 * G) for r in range(1, G)) + [n]  # uneven shards
+    hist_all = torch.stack([fs.histogram_u16(torch.from_numpy(keys[cuts[r]:cuts[r + 1]].copy()).to(cuda))
+                            for r in range(G)])
+    bounds = [(n * d) // G for d in range(G + 1)]
+    bufs = [torch.full((bounds[d + 1] - bounds[d],), 0xFFFF, dtype=torch.uint16, device=cuda) for d in range(G)]
+    for g in range(G):
+        fs.expand_to_peers_u16(hist_all, g, bufs)
+    torch.cuda.synchronize()
+    got = np.concatenate([b.cpu().numpy() for b in bufs])
+    np.testing.assert_array_equal(got, oracle.sort_u16(keys))
