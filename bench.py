@@ -250,6 +250,7 @@ def run_fs_pairs(args, dev):
     achieved = alg / (phase[dom] * 1e-3) / 1e9
     t_step = total_ms / steps
     method_b = 80 * n if path == "msd" else 200 * n
+    traffic, traffic_src = load_traffic(names[dom])
     line = {
         "metric": METRIC, "value": round(n * steps / (total_ms * 1e-3) / 1e9, 3), "unit": "Gkeys/s", "n_gpus": 1,
         "steps": steps, "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
@@ -257,9 +258,9 @@ def run_fs_pairs(args, dev):
         "config": {"workload": "c5: 536,870,912 (u64 key uniform, u32 value = index) pairs, stable ascending sort",
                    "pairs": n, "l2": "inputs (6 GiB) larger than L2: no flush", "path": path},
         "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(phase[dom], 4),
-                     "peak_source": peak_src},
+                     "peak_source": peak_src, "traffic_source": traffic_src},
         "whole_step": {"minimal_bytes": 24 * n, "method_bytes": method_b,
                        "frac_minimal_of_measured_peak": round(24 * n / (t_step * 1e-3) / 1e9 / peak, 4),
                        "method_GBps": round(method_b / (t_step * 1e-3) / 1e9, 1),

@@ -74,12 +74,18 @@ constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 // ---- MSD geometry
 constexpr int kTopBits = 16;            // bits binned by the trie (two 8-bit MSD levels)
 constexpr int kSegs = 256;              // first-level segments
-constexpr int kLocalThreads = 512;
+#ifndef FS_LOCAL_THREADS
+#define FS_LOCAL_THREADS 512
+#endif
+#ifndef FS_LOCAL_CB
+#define FS_LOCAL_CB 12
+#endif
+constexpr int kLocalThreads = FS_LOCAL_THREADS;
 constexpr int kLocalWarps = kLocalThreads / 32;
 constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in shared memory
 constexpr int kIdxBits = 14;            // local index bits of the composite key
 static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
-constexpr int kCountBitsMax = 12;       // local counting digit (<= 4,096 groups)
+constexpr int kCountBitsMax = FS_LOCAL_CB;  // local counting digit (<= 4,096 groups)
 constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 constexpr uint64_t kMsdMinN = 1ull << 22;
 
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(256)
   if (!msd->use_msd) return;
   const uint32_t v = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint4* row = reinterpret_cast<const uint4*>(partials + (uint64_t)v * kHistWords);
+#pragma unroll 8  // the loads of 8 digits in flight at once
   for (uint32_t d = warp; d < kRadix; d += 8) {
     const uint4 q = __ldcg(row + d * 32 + lane);  // 128 words = 256 leaves
     uint32_t x = (q.x & 0xFFFFu) + (q.x >> 16) + (q.y & 0xFFFFu) + (q.y >> 16) + (q.z & 0xFFFFu) + (q.z >> 16) +
@@ -305,8 +312,9 @@ __global__ void __launch_bounds__(kSegs)
     rmax = 0;
   }
   __syncthreads();
-  uint64_t mx = 0;
-  for (int j = 0; j < 256; ++j) mx = max(mx, (uint64_t)H16[s * 256 + j]);
+  uint64_t mx = 0;  // largest bin: coalesced, 16 loads in flight per thread
+#pragma unroll 16
+  for (int j = 0; j < kHistBins / kSegs; ++j) mx = max(mx, (uint64_t)__ldg(H16 + j * kSegs + s));
   if (mx > (uint64_t)kLocalCap) too_big = 1;
   const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
   const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);

@@ -67,13 +67,19 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--out", default="profiles")
     ap.add_argument("--note", default="")
+    ap.add_argument("--alias", default="", help="name#i=alias,... renames the i-th launch of a kernel")
     a = ap.parse_args()
     h, units, rows = raw(a.rep)
     lines = [f"# ncu summary {a.tag}", "", a.note, "",
              f"Source: `{os.path.basename(a.rep)}` (ncu --set full --clock-control none; caches flushed per replay).", ""]
     traffic = {}
+    alias = dict(x.split("=") for x in a.alias.split(",") if x)
+    seen = defaultdict(int)
     for r in rows:
         k = short(r[h.index("Kernel Name")])
+        kk = f"{k.replace('k_', '')}#{seen[k]}"
+        seen[k] += 1
+        k = alias.get(kk, k)
         lines.append(f"## {k}")
         lines.append("")
         lines.append("| metric | value | unit |")
