@@ -196,11 +196,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   // per-CTA loop 115-125 us on 2^28 keys).  Per-warp tickets need no CTA
   // barrier, so no warp waits on another's loads.
   constexpr uint64_t kGroupVec = (uint64_t)kUnroll * kThreads;
-  constexpr int kChunkIters = 4;
+#ifndef FS_HIST_CHUNK_ITERS  // scripts/microbench sweeps
+#define FS_HIST_CHUNK_ITERS 8
+#define FS_HIST_DYN_DIV 16
+#endif
+  constexpr int kChunkIters = FS_HIST_CHUNK_ITERS;
   constexpr uint64_t kChunkVec = (uint64_t)kChunkIters * kUnroll * 32;
   static_assert(kGroupVec % kChunkVec == 0, "chunks tile the groups");
   const uint64_t ngroups = nvec / kGroupVec;
-  const uint64_t nstatic = ngroups - ngroups / 8;
+  const uint64_t nstatic = ngroups - ngroups / FS_HIST_DYN_DIV;
   bool agg = false;
   uint32_t phase = 0;
   // v[u] = p[u * stride]; the whole warp calls this together.

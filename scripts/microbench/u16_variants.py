@@ -22,7 +22,7 @@ for rnd in range(2):
     for _ in range(5):
         L.fs_sort_keys_u16(k.data_ptr(), out.data_ptr(), n, 16, temp.data_ptr(), temp.numel(), s)
     ts = []
-    for _ in range(30):
+    for _ in range(100):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); L.fs_sort_keys_u16(k.data_ptr(), out.data_ptr(), n, 16, temp.data_ptr(), temp.numel(), s); b.record()
         ts.append((a, b))
