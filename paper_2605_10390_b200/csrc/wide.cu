@@ -697,12 +697,11 @@ struct LocalSmemLayout {
   static constexpr int ck = 0;                                      // u64[kLocalCap]
   static constexpr int perm = ck + kLocalCap * 8;                   // u16[kLocalCap]
   static constexpr int scratch = perm + kLocalCap * 2;
-  // fast path: counters u16[2^kCountBitsMax], then the final permutation u16[kLocalCap]
-  static constexpr int fin = scratch + (1 << kCountBitsMax) * 2;
+  // fast path: counters u16[2^kCountBitsMax]; the final permutation lives in `perm`
   // slow path: perm_b u16[kLocalCap], then per-warp digit offsets u16[16][256]
   static constexpr int perm_b = scratch;
   static constexpr int whist = scratch + kLocalCap * 2;
-  static constexpr int fast_end = fin + kLocalCap * 2;
+  static constexpr int fast_end = scratch + (1 << kCountBitsMax) * 2;
   static constexpr int slow_end = whist + kLocalWarps * kRadix * 2;
   static constexpr int total = fast_end > slow_end ? fast_end : slow_end;
 };
@@ -736,27 +735,26 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   const int cshift = kIdxBits + R - cb;
 
   if (tid == 0) heavy = 0;
-  for (uint32_t w = tid; w < nwords; w += kLocalThreads) cntw[w] = 0;
-  {
-    constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;  // 17: all loads in flight at once
-    K kr[kPer];
+  // Keys: all loads in flight at once, turned into composites that stay in
+  // registers; the digit histogram is counted from them; after the scan each
+  // composite is written straight to its group's slot (ck is filled in group
+  // order, never in arrival order: the arrival index is in the composite).
+  constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;  // 17
+  uint64_t cr[kPer];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const uint32_t i = tid + u * kLocalThreads;
-      kr[u] = i < m ? keys[b0 + i] : K(0);
-    }
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const uint32_t i = tid + u * kLocalThreads;
-      if (i < m) ck[i] = (((uint64_t)kr[u] & low_mask) << kIdxBits) | i;
-    }
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = tid + u * kLocalThreads;
+    cr[u] = i < m ? ((((uint64_t)keys[b0 + i]) & low_mask) << kIdxBits) | i : 0ull;
   }
+  for (uint32_t w = tid; w < nwords; w += kLocalThreads) cntw[w] = 0;
   __syncthreads();
-
-  // ---- histogram of the counting digit (u16 counters packed two per word; m < 2^16)
-  for (uint32_t i = tid; i < m; i += kLocalThreads) {
-    const uint32_t g = (uint32_t)(ck[i] >> cshift) & (ngroups - 1);
-    atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = tid + u * kLocalThreads;
+    if (i < m) {
+      const uint32_t g = (uint32_t)(cr[u] >> cshift) & (ngroups - 1);
+      atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
+    }
   }
   __syncthreads();
 
@@ -785,25 +783,25 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   }
   __syncthreads();
 
-  // ---- counting scatter of the local indices (order inside a group is fixed below)
-  for (uint32_t i = tid; i < m; i += kLocalThreads) {
-    const uint32_t g = (uint32_t)(ck[i] >> cshift) & (ngroups - 1);
-    const uint32_t old = atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
-    perm[(g & 1u) ? (old >> 16) : (old & 0xFFFFu)] = (uint16_t)i;
+  // ---- counting scatter of the composites (order inside a group is fixed below)
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = tid + u * kLocalThreads;
+    if (i < m) {
+      const uint32_t g = (uint32_t)(cr[u] >> cshift) & (ngroups - 1);
+      const uint32_t old = atomicAdd(&cntw[g >> 1], (g & 1u) ? 0x10000u : 1u);
+      ck[(g & 1u) ? (old >> 16) : (old & 0xFFFFu)] = cr[u];
+    }
   }
   __syncthreads();
 
   // ---- final positions: group start + rank of the composite inside its group
-  //      (cnt16[g] = end of group g).  Lane j of a warp holds sorted slot j, so
-  //      the members of its group sit in neighbouring lanes: they are compared
-  //      through shuffles; members outside the warp's 32 slots (a group cut by
-  //      the chunk edge) through shared memory.  Keys go straight to the output;
-  //      (element, position) pairs stay in registers until perm is free.
+  //      (cnt16[g] = end of group g); keys go straight to the output, the
+  //      arrival index of every position to fin (= perm).
   const K top = (K)((uint64_t)bkt << R);
-  uint16_t* fin = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::fin);
+  uint16_t* fin = perm;
   for (uint32_t j = tid; j < m; j += kLocalThreads) {
-    const uint16_t p = perm[j];
-    const uint64_t c = ck[p];
+    const uint64_t c = ck[j];
     const uint32_t g = (uint32_t)(c >> cshift) & (ngroups - 1);
     const uint32_t s0 = g ? cnt16[g - 1] : 0u, e = cnt16[g];
     if (e - s0 > (uint32_t)kMaxGroup) {
@@ -811,10 +809,9 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
       continue;
     }
     uint32_t r = s0;
-    for (uint32_t k = s0; k < e; ++k)
-      if (k != j) r += ck[perm[k]] < c;
+    for (uint32_t k = s0; k < e; ++k) r += ck[k] < c;
     keys[b0 + r] = top | (K)(c >> kIdxBits);
-    fin[r] = p;
+    fin[r] = (uint16_t)(c & ((1u << kIdxBits) - 1));
   }
   __syncthreads();
 
@@ -830,11 +827,12 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
     }
     __syncthreads();
     unsigned long long o = 0, an = ~0ull;
-    for (uint32_t i = tid; i < m; i += kLocalThreads) {
-      const uint64_t v = ck[i] >> kIdxBits;
+    for (uint32_t j = tid; j < m; j += kLocalThreads) {  // ck is in group order: pa lists it in arrival order
+      const uint64_t c = ck[j];
+      const uint64_t v = c >> kIdxBits;
       o |= v;
       an &= v;
-      pa[i] = (uint16_t)i;  // arrival order
+      pa[c & ((1u << kIdxBits) - 1)] = (uint16_t)j;
     }
     atomicOr(&or_all, o);
     atomicAnd(&and_all, an);
@@ -903,12 +901,16 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   }
 
   // ---- write the bin back in sorted order (the fast path has written the keys)
-  if (heavy)
-    for (uint32_t j = tid; j < m; j += kLocalThreads) keys[b0 + j] = top | (K)(ck[pfinal[j]] >> kIdxBits);
+  if (heavy) {  // pfinal lists ck slots: write the keys, then turn it into arrival indices for the values
+    for (uint32_t j = tid; j < m; j += kLocalThreads) {
+      const uint64_t c = ck[pfinal[j]];
+      keys[b0 + j] = top | (K)(c >> kIdxBits);
+      pfinal[j] = (uint16_t)(c & ((1u << kIdxBits) - 1));
+    }
+  }
   if (kHasValues) {
-    __syncthreads();  // ck is free: stage the values there
+    __syncthreads();  // ck is free: stage the values there (arrival order)
     uint32_t* sv = reinterpret_cast<uint32_t*>(ck);
-    constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;
     uint32_t vr[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
