@@ -45,6 +45,10 @@
 #include "kernels.cuh"
 #include "tma.cuh"
 
+#ifdef FS_SCATTER_STATS  // scripts/microbench/scatter_stats.cu: lookback behaviour per mode
+__device__ unsigned long long g_scatter_stats[3][4];  // [mode][lookbacks, rounds, polls, inc_at_first]
+#endif
+
 namespace fs {
 namespace {
 
@@ -522,7 +526,9 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     const int cur = it & 1;
     const TileInfo ti = sm.info[cur];
     if (ti.tile == kNoTile) break;
+#ifndef FS_SCATTER_LATE_FETCH
     if (tid == 0) fetch(cur ^ 1);  // prefetch the next tile while this one is processed
+#endif
     K* kbuf = sm.keys[cur];
     uint32_t* vbuf = kHasValues ? sm.vals[cur] : nullptr;
     const uint32_t len = (uint32_t)(ti.end - ti.begin);
@@ -598,6 +604,12 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       if (lane == 31) sm.wsum[warp] = inc;
       sm.digit_start[d] = inc - cnt;  // warp-local for now
     }
+#ifdef FS_SCATTER_LATE_FETCH
+    // The next ticket is taken only once this tile's counts are published: a
+    // ticket held unstarted behind a busy tile would stall its successors'
+    // lookbacks.
+    if (tid == 0) fetch(cur ^ 1);
+#endif
     __syncthreads();
     uint32_t dstart = 0;
     if (d < kRadix) {
@@ -629,10 +641,23 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
 #else
       if (!ti.first) {
 #endif
-        constexpr int kLook = 8;
         const int64_t step = ti.stride;
         int64_t t = (int64_t)ti.tile - step;  // the segment's first tile publishes inclusive: the walk stops there
+        // The immediate predecessor almost always holds its inclusive prefix by
+        // now (scripts/microbench/scatter_stats.cu: 85-98%), so read it alone
+        // first; a window of 8 older words only when it does not.  (Always
+        // reading 8 rows cost ~16 KB of status traffic per tile, mostly DRAM:
+        // the older rows have left L2.)
         bool done = false;
+        {
+          unsigned long long s = ld_relaxed_u64(a.status + (uint64_t)t * kRadix + d);
+          while ((s & (0x3Full << kTagShift)) != a.tag || (s >> 62) == 0)  // not yet published
+            s = ld_relaxed_u64(a.status + (uint64_t)t * kRadix + d);
+          excl += s & kStValue;
+          done = (s >> 62) == 2;
+          t -= step;
+        }
+        constexpr int kLook = 8;
         while (!done) {
           unsigned long long sv[kLook];
 #pragma unroll

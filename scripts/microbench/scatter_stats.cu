@@ -1,0 +1,29 @@
+// Lookback statistics of k_scatter on c5 (2^29 pairs), per pass mode: digit-threads
+// x tiles that looked back, rounds of 8 loads, polls of unpublished words, and
+// how often the immediate predecessor already held the inclusive prefix.
+// Build: see scripts/microbench/README (objects compiled with -DFS_SCATTER_STATS -dc).
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "fractalsort.h"
+extern __device__ unsigned long long g_scatter_stats[3][4];
+__device__ __forceinline__ unsigned long long sm64(unsigned long long z){z+=0x9E3779B97F4A7C15ull;z=(z^(z>>30))*0xBF58476D1CE4E5B9ull;z=(z^(z>>27))*0x94D049BB133111EBull;return z^(z>>31);}
+__global__ void gen(unsigned long long* k, unsigned* v, unsigned long long n){ for(unsigned long long i=blockIdx.x*(unsigned long long)blockDim.x+threadIdx.x;i<n;i+=(unsigned long long)gridDim.x*blockDim.x){k[i]=sm64(i);v[i]=(unsigned)i;} }
+int main(){
+  const unsigned long long n = 1ull << 29;
+  unsigned long long *k,*ko; unsigned *v,*vo; void* t;
+  size_t tb = fs_sort_pairs_u64_u32_temp_bytes(n, 64);
+  cudaMalloc(&k,n*8); cudaMalloc(&ko,n*8); cudaMalloc(&v,n*4); cudaMalloc(&vo,n*4); cudaMalloc(&t,tb);
+  gen<<<1184,256>>>(k,v,n); cudaDeviceSynchronize();
+  for (int rep=0; rep<2; ++rep) {
+    unsigned long long z[3][4] = {};
+    cudaMemcpyToSymbol(g_scatter_stats, z, sizeof(z));
+    fs_status s = fs_sort_pairs_u64_u32((const uint64_t*)k, v, (uint64_t*)ko, vo, n, 64, t, tb, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(z, g_scatter_stats, sizeof(z));
+    printf("rep %d status %d\n", rep, (int)s);
+    for (int m = 1; m < 3; ++m)
+      printf("  mode %d: lookbacks %llu  rounds/lookback %.3f  polls/lookback %.3f  inc-at-first %.3f\n", m, z[m][0],
+             (double)z[m][1] / z[m][0], (double)z[m][2] / z[m][0], (double)z[m][3] / z[m][0]);
+  }
+  return 0;
+}
