@@ -395,7 +395,6 @@ def run_fs(args, rank, world, local_rank):
     alg_bytes = 2 * (n if world == 1 else (b1 - b0) if dom == "expand16" else n)
     peak, peak_src = measured_peak_gbs()
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    # the committed ncu capture is of c2 (per-launch DRAM bytes of that workload only)
     traffic, traffic_src = load_traffic(dom.split("+")[0]) if (args.workload == "c2" and world == 1) else (None, None)
     whole_bytes = 4 * n
     line = {
