@@ -49,4 +49,10 @@ FS_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* ba
       : "memory");
 }
 
+// Bulk prefetch of [src, src + bytes) into L2 (no completion tracking).
+// src 16-byte aligned, bytes a multiple of 16.
+FS_DEVINL void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 }  // namespace fs

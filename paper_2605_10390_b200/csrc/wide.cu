@@ -47,6 +47,19 @@
 
 #ifdef FS_SCATTER_STATS  // scripts/microbench/scatter_stats.cu: lookback behaviour per mode
 __device__ unsigned long long g_scatter_stats[3][4];  // [mode][lookbacks, rounds, polls, inc_at_first]
+__device__ unsigned long long g_scatter_phase[3][8];  // [mode][phase] clock cycles summed over CTAs (thread 0)
+#define FS_PH(i)                                                            \
+  do {                                                                     \
+    if (tid == 0) {                                                        \
+      const long long now_ = clock64();                                    \
+      atomicAdd(&g_scatter_phase[a.mode][i], (unsigned long long)(now_ - ph_t0)); \
+      ph_t0 = now_;                                                        \
+    }                                                                      \
+  } while (0)
+#else
+#define FS_PH(i) \
+  do {           \
+  } while (0)
 #endif
 
 namespace fs {
@@ -396,6 +409,7 @@ struct ScatterSmem {
   uint32_t digit_start[kRadix];      // tile-local exclusive scan over digits
   unsigned long long gofs[kRadix];   // global offset - digit_start
   uint32_t seg_tile0[kSegs + 1];
+  uint64_t seg_begin[kSegs + 1];
   uint32_t wsum[kRadix / 32];
   uint64_t mbar[2];
   TileInfo info[2];
@@ -446,56 +460,66 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
   const uint64_t n = a.n;
   const uint64_t n_al = n & ~(uint64_t)3;  // bulk copies never read past this
 
+  // Tile of a ticket (shared-memory reads only): false for a hole.
+  auto decode = [&](uint32_t tk, TileInfo& t) -> bool {
+    t.tile = tk;
+    t.stride = inter ? nseg : 1u;
+    uint32_t r;
+    uint64_t sb, se;
+    if (inter) {
+      t.seg = tk % nseg;
+      r = tk / nseg;
+      if (a.mode == 1) {
+        sb = (uint64_t)t.seg * a.l1_chunk_tiles * kSTile;
+        se = min(sb + (uint64_t)a.l1_chunk_tiles * kSTile, n);
+      } else {
+        if (r >= sm.seg_tile0[t.seg + 1] - sm.seg_tile0[t.seg]) return false;  // segment has fewer tiles
+        sb = sm.seg_begin[t.seg];
+        se = sm.seg_begin[t.seg + 1];
+      }
+      if (sb + (uint64_t)r * kSTile >= se) return false;
+    } else if (a.mode == 2) {
+      uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile (a non-empty segment)
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sm.seg_tile0[mid] <= tk) lo = mid; else hi = mid;
+      }
+      t.seg = lo;
+      r = tk - sm.seg_tile0[lo];
+      sb = sm.seg_begin[lo];
+      se = sm.seg_begin[lo + 1];
+    } else {
+      t.seg = 0;
+      r = tk;
+      sb = 0;
+      se = n;
+    }
+    t.first = r == 0;
+    t.begin = sb + (uint64_t)r * kSTile;
+    t.end = min(t.begin + (uint64_t)kSTile, se);
+    t.abeg = a.tma ? (t.begin & ~(uint64_t)3) : t.begin;
+    return true;
+  };
   // Thread 0: take the next tile, describe it, and (with TMA) start its copy.
+  // Tickets are requested one tile ahead (`spare`): the atomic's round trip
+  // overlaps a whole tile instead of stalling thread 0 at every iteration.
+  uint32_t spare = 0;
   auto fetch = [&](int buf) {
     TileInfo t;
-    t.stride = inter ? nseg : 1u;
     for (;;) {
-      t.tile = atomicAdd(a.ticket, 1u);
-      if (t.tile >= ntiles) {
+      const uint32_t tk = spare;
+      spare = atomicAdd(a.ticket, 1u);
+      if (tk >= ntiles) {
         t.tile = kNoTile;
         t.begin = t.end = t.abeg = 0;
         t.seg = 0;
         t.first = 0;
+        t.stride = 1;
         sm.info[buf] = t;
         return;
       }
-      uint32_t r;
-      uint64_t sb, se;
-      if (inter) {
-        t.seg = t.tile % nseg;
-        r = t.tile / nseg;
-        if (a.mode == 1) {
-          sb = (uint64_t)t.seg * a.l1_chunk_tiles * kSTile;
-          se = min(sb + (uint64_t)a.l1_chunk_tiles * kSTile, n);
-        } else {
-          if (r >= sm.seg_tile0[t.seg + 1] - sm.seg_tile0[t.seg]) continue;  // hole: segment has fewer tiles
-          sb = __ldcg(&a.msd->seg_begin[t.seg]);
-          se = __ldcg(&a.msd->seg_begin[t.seg + 1]);
-        }
-        if (sb + (uint64_t)r * kSTile >= se) continue;  // hole
-      } else if (a.mode == 2) {
-        uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile (a non-empty segment)
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (sm.seg_tile0[mid] <= t.tile) lo = mid; else hi = mid;
-        }
-        t.seg = lo;
-        r = t.tile - sm.seg_tile0[lo];
-        sb = __ldcg(&a.msd->seg_begin[lo]);
-        se = __ldcg(&a.msd->seg_begin[lo + 1]);
-      } else {
-        t.seg = 0;
-        r = t.tile;
-        sb = 0;
-        se = n;
-      }
-      t.first = r == 0;
-      t.begin = sb + (uint64_t)r * kSTile;
-      t.end = min(t.begin + (uint64_t)kSTile, se);
-      break;
+      if (decode(tk, t)) break;
     }
-    t.abeg = a.tma ? (t.begin & ~(uint64_t)3) : t.begin;
     sm.info[buf] = t;
     if (a.tma) {
       const uint64_t aend = min((t.end + 3) & ~(uint64_t)3, n_al);
@@ -508,6 +532,17 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       }
     }
   };
+  // Thread 0: warm L2 with the tile after next (the spare ticket) so the bulk
+  // copy issued for it one tile later finds its bytes on chip.
+  auto prefetch_spare = [&]() {
+    TileInfo t;
+    if (!a.tma || spare >= ntiles || !decode(spare, t)) return;
+    const uint64_t aend = min((t.end + 3) & ~(uint64_t)3, n_al);
+    if (aend <= t.abeg) return;
+    const uint32_t cnt = (uint32_t)(aend - t.abeg);
+    bulk_prefetch_l2(src_k + t.abeg, cnt * (uint32_t)sizeof(K));
+    if (kHasValues) bulk_prefetch_l2(src_v + t.abeg, cnt * 4u);
+  };
 
   if (tid == 0) {
     mbar_init(&sm.mbar[0], 1);
@@ -515,13 +550,22 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     mbar_fence_init();
   }
   if (a.mode == 2)
-    for (int i = tid; i <= kSegs; i += kSThreads) sm.seg_tile0[i] = __ldcg(&a.msd->seg_tile0[i]);
+    for (int i = tid; i <= kSegs; i += kSThreads) {
+      sm.seg_tile0[i] = __ldcg(&a.msd->seg_tile0[i]);
+      sm.seg_begin[i] = __ldcg(&a.msd->seg_begin[i]);
+    }
   for (int i = tid; i < kSWarps * kRadix / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
   __syncthreads();
-  if (tid == 0) fetch(0);
+  if (tid == 0) {
+    spare = atomicAdd(a.ticket, 1u);
+    fetch(0);
+  }
   __syncthreads();
 
   const int shift = a.shift;
+#ifdef FS_SCATTER_STATS
+  long long ph_t0 = clock64();
+#endif
   for (uint32_t it = 0;; ++it) {
     const int cur = it & 1;
     const TileInfo ti = sm.info[cur];
@@ -557,6 +601,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     const uint32_t d = tid;
     const uint64_t dbase = d < kRadix ? __ldg(base_tab + (uint64_t)ti.seg * base_ss + (uint64_t)d * base_ds) : 0ull;
 
+    FS_PH(0);  // 0: fetch + wait for the tile's bytes
     // ---- items: warp w holds tile elements [256 w, 256 w + 256), item i of lane l = 256 w + 32 i + l
     K key[kSItems];
     uint32_t val[kHasValues ? kSItems : 1];
@@ -588,6 +633,8 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     }
     __syncthreads();
 
+    if (tid == 0) prefetch_spare();
+    FS_PH(1);  // 1: load items + rank + barrier
     // ---- tile digit counts (thread = digit); publish; per-warp offsets
     uint32_t cnt = 0;
     unsigned long long* st = a.status + (uint64_t)ti.tile * kRadix + d;
@@ -623,6 +670,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     }
     __syncthreads();
 
+    FS_PH(2);  // 2: counts, publish, digit scan, offsets (2 barriers)
     // ---- reorder through shared memory (the tile's input buffer becomes the stage)
 #pragma unroll
     for (int i = 0; i < kSItems; ++i) {
@@ -633,6 +681,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       }
     }
 
+    FS_PH(3);  // 3: reorder stores (thread 0's share)
     // ---- decoupled lookback over earlier tiles of the segment (thread = digit)
     if (d < kRadix) {
       unsigned long long excl = 0;
@@ -681,6 +730,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     }
     __syncthreads();
 
+    FS_PH(4);  // 4: lookback + barrier
     // ---- scatter: consecutive positions of one digit go to consecutive addresses
     for (uint32_t j = tid; j < len; j += kSThreads) {
       const K k = kbuf[j];
@@ -689,7 +739,9 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       if (kHasValues) dst_v[dst] = vbuf[j];
     }
     for (int i = tid; i < kSWarps * kRadix / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
+    FS_PH(5);  // 5: scatter stores (thread 0's share)
     __syncthreads();  // the stage (this buffer) is free for the prefetch after next
+    FS_PH(6);  // 6: end barrier
   }
 }
 
