@@ -7,12 +7,16 @@ sys.path.insert(0, ROOT)
 import datagen
 
 n = 1 << 28
+dist = sys.argv[1] if len(sys.argv) > 1 else "uniform"
 dev = torch.device("cuda", 0)
 s = torch.cuda.current_stream().cuda_stream
 k = torch.empty(n, dtype=torch.uint16, device=dev)
-datagen.gen_u16_device(k.data_ptr(), "uniform", n, seed=0, stream=s)
+if dist == "sortedswap":
+    k.copy_(torch.from_numpy(datagen.gen_u16("sortedswap", n, seed=0)))
+else:
+    datagen.gen_u16_device(k.data_ptr(), dist, n, seed=0, stream=s)
 out = torch.empty_like(k)
-for rnd in range(2):
+for rnd in range(1):
   for path in sorted(glob.glob(os.path.join(ROOT, "scripts/microbench/variants/*.so"))):
     L = ctypes.CDLL(path)
     L.fs_sort_keys_u16_temp_bytes.restype = ctypes.c_size_t
@@ -29,4 +33,4 @@ for rnd in range(2):
     torch.cuda.synchronize()
     t = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
     ok = bool((out[1:].to(torch.int32) >= out[:-1].to(torch.int32)).all().item())
-    print(f"{os.path.basename(path):24s} median {t[len(t)//2]:7.2f} us  min {t[0]:7.2f}  sorted={ok}", flush=True)
+    print(f"{dist:10s} {os.path.basename(path):24s} median {t[len(t)//2]:7.2f} us  min {t[0]:7.2f}  sorted={ok}", flush=True)
