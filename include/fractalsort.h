@@ -165,6 +165,15 @@ fs_status fs_expand_u16(const uint64_t* prefix, uint64_t nbins, uint64_t out_beg
 fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                          fs_stream_t stream);
 
+/* fs_bound_u64: out[i] = #{j : sorted[j] < queries[i]} (upper = 0, the lower
+ * bound) or #{j : sorted[j] <= queries[i]} (upper = 1) for an ascending u64
+ * array of n keys on the device; q queries, one thread each.  The rank counts
+ * behind the exact, sampling-free splitters of the distributed pair sort
+ * (SURVEY.md §8(e) Mode A for pairs; GetIndex, Alg. 3, on a
+ * sorted shard).  out must not overlap the inputs. */
+fs_status fs_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* queries, uint64_t q, int upper,
+                       uint64_t* out, fs_stream_t stream);
+
 /* fs_expand_to_peers_u16: the fused exchange of the multi-GPU keys-only sort
  * (SURVEY.md §8(f) NEXT-2): rank g writes each of its own keys straight to its
  * final global sorted position, in the output buffer of the rank that owns it.

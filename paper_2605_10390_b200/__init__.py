@@ -21,7 +21,7 @@ from ._lib import FractalSortError, check, lib
 __all__ = [
     "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
-    "expand_to_peers_u16", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
+    "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
 ]
 
 _TEMP_ALIGN = 256
@@ -159,6 +159,16 @@ def send_counts(hist_all: torch.Tensor, g: int) -> torch.Tensor:
         check(lib().fs_send_counts(hist_all.data_ptr(), G, g, nb, send.data_ptr(), _stream(dev)),
               "fs_send_counts")
     return send
+
+
+def bound_u64(sorted_keys: torch.Tensor, queries: torch.Tensor, upper: bool = False) -> torch.Tensor:
+    """#keys < q (upper=False) or <= q (upper=True) in an ascending uint64 tensor (fs_bound_u64)."""
+    dev = _require_cuda(sorted_keys, queries)
+    out = torch.empty(queries.numel(), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_bound_u64(sorted_keys.data_ptr(), sorted_keys.numel(), queries.data_ptr(), queries.numel(),
+                                 int(bool(upper)), out.data_ptr(), _stream(dev)), "fs_bound_u64")
+    return out
 
 
 def expand_to_peers_u16(hist_all: torch.Tensor, g: int, dest: list) -> None:

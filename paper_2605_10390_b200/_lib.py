@@ -36,6 +36,7 @@ SIGNATURES = {
     "fs_sort_keys_u16_host_work_bytes": (_sz, [_u64, _u64]),
     "fs_sort_keys_u16_host": (_i32, [_vp, _vp, _u64, _u64, _vp, _sz, _vp]),
     "fs_set_phase_events": (_i32, [_vp, _i32]),
+    "fs_bound_u64": (_i32, [_vp, _u64, _vp, _u64, _i32, _vp, _vp]),
     "fs_expand_to_peers_u16_temp_bytes": (_sz, [_u64, _i32]),
     "fs_expand_to_peers_u16": (_i32, [_vp, _i32, _i32, _u64, _vp, _vp, _sz, _vp]),
     "fs_trie_levels_count": (_sz, [_i32]),

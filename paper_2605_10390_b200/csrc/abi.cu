@@ -264,6 +264,20 @@ fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins,
   return finish(s, "fs_send_counts");
 }
 
+fs_status fs_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* queries, uint64_t q, int upper,
+                       uint64_t* out, fs_stream_t stream) {
+  clear_error();
+  if (q == 0) return FS_OK;
+  if (!queries || !out || (n && !sorted)) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (upper != 0 && upper != 1) return fail(FS_ERR_INVALID_ARGUMENT, "upper must be 0 or 1");
+  if (overlaps(queries, q * 8, out, q * 8) || (n && overlaps(sorted, n * 8, out, q * 8)))
+    return fail(FS_ERR_INVALID_ARGUMENT, "out overlaps an input");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_bound_u64(sorted, n, queries, q, upper, out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_bound_u64");
+  return finish(s, "fs_bound_u64");
+}
+
 // ------------------------------------------------------------ NEXT-2: fused expand-to-peer
 size_t fs_expand_to_peers_u16_temp_bytes(uint64_t nbins, int G) {
   return (nbins == 0 || nbins > 65536 || G < 1 || G > 1024) ? 0 : expand_to_peers_temp_bytes(nbins, G);

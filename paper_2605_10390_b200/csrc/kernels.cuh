@@ -56,6 +56,9 @@ cudaError_t launch_expand16_two_level(const uint64_t* slice_prefix, const uint64
 cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                                cudaStream_t s);
 
+cudaError_t launch_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* q, uint64_t nq, int upper,
+                             uint64_t* out, cudaStream_t s);
+
 // ---------------------------------------------------------------- peer.cu
 size_t expand_to_peers_temp_bytes(uint64_t nbins, int G);
 cudaError_t launch_expand_to_peers(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest_host,

@@ -91,3 +91,34 @@ cudaError_t launch_send_counts(const uint64_t* hist_all, int G, int g, uint64_t 
 }
 
 }  // namespace fs
+
+// ---------------------------------------------------------------------------
+// Exact splitters of the distributed pair sort (SURVEY.md §8(e) Mode A for
+// pairs): the rank of a probe key in a rank's locally sorted keys.
+// out[i] = #{j : sorted[j] < q[i]} (upper = 0) or #{j : sorted[j] <= q[i]}
+// (upper = 1): one thread per probe, binary search over the sorted shard.
+namespace fs {
+namespace {
+__global__ void __launch_bounds__(256) k_bound_u64(const uint64_t* __restrict__ sorted, uint64_t n,
+                                                   const uint64_t* __restrict__ q, uint64_t nq, int upper,
+                                                   uint64_t* __restrict__ out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  const uint64_t x = q[i];
+  uint64_t lo = 0, hi = n;  // first index whose key is >= x (lower) / > x (upper)
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    const uint64_t k = __ldg(sorted + mid);
+    if (upper ? (k <= x) : (k < x)) lo = mid + 1; else hi = mid;
+  }
+  out[i] = lo;
+}
+}  // namespace
+
+cudaError_t launch_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* q, uint64_t nq, int upper,
+                             uint64_t* out, cudaStream_t s) {
+  if (nq == 0) return cudaSuccess;
+  k_bound_u64<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(sorted, n, q, nq, upper, out);
+  return cudaGetLastError();
+}
+}  // namespace fs

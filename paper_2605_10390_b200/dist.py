@@ -55,6 +55,14 @@ class CudaOps:
         from . import send_counts
         return send_counts(hist_all, g)             # int64[G]
 
+    def sort_pairs(self, keys, vals):
+        from . import sort_pairs
+        return sort_pairs(keys, vals)
+
+    def bound_u64(self, sorted_keys, queries, upper):
+        from . import bound_u64
+        return bound_u64(sorted_keys, queries, upper)            # int64 counts
+
     def expand_to_peers(self, hist_all, g, dest):
         from . import expand_to_peers_u16
         expand_to_peers_u16(hist_all, g, dest)
@@ -149,3 +157,85 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         dist.barrier(group=group)                              # every producer has finished writing
         return dest[rank][:end - begin], (begin, end)
     raise ValueError(f"unknown mode {mode!r}")
+
+
+# ---------------------------------------------------------------- pairs (Mode A)
+def _u64_tensor(values, device):
+    import numpy as np
+    return torch.from_numpy(np.array(values, dtype=np.uint64).view(np.int64)).to(device).view(torch.uint64)
+
+
+def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=None, key_bits: int = 64):
+    """Stable sort of the (u64 key, u32 value) pairs of all ranks (SURVEY.md §8(e)
+    Mode A for pairs): the ranks' shards are contiguous slices of the input in
+    rank order, so the global stable order breaks key ties by (rank, local
+    position).  Returns (this rank's slice of the sorted pairs, (begin, end)).
+
+    1. stable local sort of the shard;
+    2. exact splitters, no sampling: for every rank boundary s_d = floor(dN/G)
+       the key K_d of the element at global position s_d is found by bisection
+       over the key space, each step one fs_bound_u64 (rank counts) and one
+       all_reduce; ties at K_d are split by source rank (ledger 13, 23);
+    3. all_to_all of keys and values by those cuts (the payload exchange);
+    4. stable local sort of what arrived (runs arrive in source-rank order).
+    """
+    if keys.dtype != torch.uint64 or vals.dtype != torch.uint32 or keys.numel() != vals.numel():
+        raise TypeError("uint64 keys and uint32 values of equal length expected")
+    ops = ops or CudaOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = keys.device
+    n_local = keys.numel()
+    sizes = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    all_sizes = [torch.empty_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    N = int(sum(int(t.item()) for t in all_sizes))
+    begin, end = output_range(rank, world, N)
+    ks, vs = ops.sort_pairs(keys, vals) if n_local else (keys, vals)
+    if world == 1:
+        return (ks, vs), (begin, end)
+    bounds = [(N * d) // world for d in range(1, world)]       # s_d, d = 1 .. G-1
+    lo = [0] * (world - 1)
+    hi = [(1 << key_bits) - 1] * (world - 1)
+    while any(l < h for l, h in zip(lo, hi)):
+        mid = [l + (h - l) // 2 for l, h in zip(lo, hi)]
+        cnt = ops.bound_u64(ks, _u64_tensor(mid, dev), True)     # local #keys <= mid
+        dist.all_reduce(cnt, group=group)
+        c = [int(x) for x in cnt.tolist()]
+        for d in range(world - 1):
+            if lo[d] < hi[d]:
+                if c[d] <= bounds[d]:
+                    lo[d] = mid[d] + 1
+                else:
+                    hi[d] = mid[d]
+    K = _u64_tensor(lo, dev)
+    below = ops.bound_u64(ks, K, False)                          # local #keys < K_d
+    equal = ops.bound_u64(ks, K, True) - below                   # local #keys == K_d
+    mine = torch.stack([below, equal])                           # 2 x (G-1)
+    gathered = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(gathered, mine, group=group)
+    allb = torch.stack(gathered).cpu().tolist()                 # [rank][below/equal][d]
+    cuts = [0]
+    for d in range(world - 1):
+        L = sum(allb[r][0][d] for r in range(world))
+        t = bounds[d] - L                                        # ties at K_d before the boundary
+        before = sum(allb[r][1][d] for r in range(rank))
+        take = min(max(t - before, 0), allb[rank][1][d])
+        cuts.append(allb[rank][0][d] + take)
+    cuts.append(n_local)
+    send = [cuts[d + 1] - cuts[d] for d in range(world)]
+    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    recv_t = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv_t, send_t, group=group)
+    recv = [int(x) for x in recv_t.tolist()]
+    assert sum(recv) == end - begin
+    rk = torch.empty(end - begin, dtype=torch.uint64, device=dev)
+    rv = torch.empty(end - begin, dtype=torch.uint32, device=dev)
+    # NCCL / gloo have no unsigned 64/32-bit types: exchange the same bytes as int64 / int32
+    dist.all_to_all_single(rk.view(torch.int64), ks.view(torch.int64), output_split_sizes=recv,
+                           input_split_sizes=send, group=group)
+    dist.all_to_all_single(rv.view(torch.int32), vs.view(torch.int32), output_split_sizes=recv,
+                           input_split_sizes=send, group=group)
+    if rk.numel():
+        rk, rv = ops.sort_pairs(rk, rv)
+    return (rk, rv), (begin, end)

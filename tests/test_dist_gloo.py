@@ -67,6 +67,16 @@ class OracleOps:
     def synchronize(self, device):
         pass
 
+    def sort_pairs(self, keys, vals):
+        import oracle
+        k, v = oracle.sort_pairs_u64_u32(keys.numpy(), vals.numpy())
+        return torch.from_numpy(k), torch.from_numpy(v)
+
+    def bound_u64(self, sorted_keys, queries, upper):
+        # a library routine stands in for fs_bound_u64 on CPU
+        return torch.from_numpy(np.searchsorted(sorted_keys.numpy(), queries.numpy(),
+                                                side="right" if upper else "left").astype(np.int64))
+
 
 class SharedPeers:
     """CPU stand-in of dist.PeerBuffers: shared-memory buffers made by the parent."""
@@ -149,3 +159,57 @@ def test_output_range_helper():
     assert ranges[0][0] == 0 and ranges[-1][1] == n
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(3))
     assert sorted(e - b for b, e in ranges) == [4, 4, 4, 5]
+
+
+PAIR_CASES = [("uniform", False), ("ties8", True), ("const", False), ("ties3", True)]
+N_PAIRS = 20_011
+
+
+def pair_input(kind):
+    import datagen
+    k = datagen.gen_u64(N_PAIRS, seed=9)
+    if kind == "ties8":
+        k = k & np.uint64(7)          # ties straddle every rank boundary
+    elif kind == "ties3":
+        k = (k % np.uint64(3)) << np.uint64(62)
+    elif kind == "const":
+        k = np.full(N_PAIRS, 0xFEDCBA9876543210, dtype=np.uint64)
+    return k, datagen.iota_u32(N_PAIRS)
+
+
+def pair_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    from paper_2605_10390_b200 import dist as fsdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for ci, (kind, uneven) in enumerate(PAIR_CASES):
+            b, e = shard_bounds(N_PAIRS, world, rank, uneven)
+            k, v = pair_input(kind)
+            (ok, ov), (ob, oe) = fsdist.sort_pairs_u64_u32(torch.from_numpy(k[b:e].copy()),
+                                                           torch.from_numpy(v[b:e].copy()), ops=OracleOps())
+            np.save(os.path.join(outdir, f"pk_{ci}_{rank}.npy"), ok.numpy())
+            np.save(os.path.join(outdir, f"pv_{ci}_{rank}.npy"), ov.numpy())
+            np.save(os.path.join(outdir, f"pr_{ci}_{rank}.npy"), np.array([ob, oe], dtype=np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_distributed_pairs_match_oracle(tmp_path, world):
+    """Mode A for pairs: exact splitters by bisection + tie split by source rank,
+    all_to_all, stable local re-sort.  The concatenated slices equal the oracle's
+    stable sort of the whole input (values = arrival indices: stability checked)."""
+    import oracle
+    mp.start_processes(pair_worker, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for ci, (kind, uneven) in enumerate(PAIR_CASES):
+        ks = [np.load(tmp_path / f"pk_{ci}_{r}.npy") for r in range(world)]
+        vs = [np.load(tmp_path / f"pv_{ci}_{r}.npy") for r in range(world)]
+        ranges = [tuple(np.load(tmp_path / f"pr_{ci}_{r}.npy")) for r in range(world)]
+        assert ranges == [((N_PAIRS * d) // world, (N_PAIRS * (d + 1)) // world) for d in range(world)]
+        k, v = pair_input(kind)
+        ek, ev = oracle.sort_pairs_u64_u32(k, v)
+        np.testing.assert_array_equal(np.concatenate(ks), ek, err_msg=f"{kind} world={world}")
+        np.testing.assert_array_equal(np.concatenate(vs), ev, err_msg=f"{kind} world={world}")

@@ -56,3 +56,28 @@ def test_expand_to_peers_virtual_ranks(cuda, G, dist_name):
     torch.cuda.synchronize()
     got = np.concatenate([b.cpu().numpy() for b in bufs])
     np.testing.assert_array_equal(got, oracle.sort_u16(keys))
+
+
+@pytest.mark.parametrize("n", [0, 1, 1000, 1_000_003])
+def test_bound_u64_matches_searchsorted(cuda, n):
+    """fs_bound_u64 (splitter rank counts) = #keys < q / <= q, checked against
+    numpy.searchsorted on the same ascending array (duplicates, extremes)."""
+    import paper_2605_10390_b200 as fs
+    k = np.sort(datagen.gen_u64(n, seed=3) & np.uint64(0xFFFF0000000000FF)) if n else np.zeros(0, np.uint64)
+    q = np.concatenate([datagen.gen_u64(500, seed=4), k[:: max(1, n // 100)][:200],
+                        np.array([0, 2**64 - 1], dtype=np.uint64)]).astype(np.uint64)
+    kd = torch.from_numpy(k).to(cuda)
+    qd = torch.from_numpy(q).to(cuda)
+    for upper, side in ((False, "left"), (True, "right")):
+        got = fs.bound_u64(kd, qd, upper).cpu().numpy()
+        np.testing.assert_array_equal(got, np.searchsorted(k, q, side=side).astype(np.int64))
+
+
+def test_dist_pairs_single_rank(cuda, nccl_group):
+    k = datagen.gen_u64(500_001, seed=5) & np.uint64(0xFF)
+    v = datagen.iota_u32(500_001)
+    (ko, vo), (b, e) = fsdist.sort_pairs_u64_u32(torch.from_numpy(k).to(cuda), torch.from_numpy(v).to(cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    assert (b, e) == (0, k.size)
+    np.testing.assert_array_equal(ko.cpu().numpy(), ek)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
