@@ -547,14 +547,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if os.environ.get("FS_BENCH_SHARE_GPU") == "1":
+        # plumbing check of the N > 1 code path on a one-GPU box (every rank on
+        # device 0, gloo collectives); its numbers mean nothing
+        local_rank = 0
     if world > 1:
         import datetime
 
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", timeout=datetime.timedelta(seconds=600),
-                                device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FS_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, timeout=datetime.timedelta(seconds=600),
+                                device_id=torch.device("cuda", local_rank) if backend == "nccl" else None)
     try:
         run_fs(args, rank, world, local_rank)
     finally:
