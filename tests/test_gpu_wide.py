@@ -171,3 +171,47 @@ def test_msd_unaligned_buffers(cuda):
     ek, ev = oracle.sort_pairs_u64_u32(k[1:], v[1:])
     np.testing.assert_array_equal(to_host(ko), ek)
     np.testing.assert_array_equal(to_host(vo), ev)
+
+
+def _fuzz_keys(rng, n, key_bits, kind):
+    k = datagen.gen_u64(n, seed=int(rng.integers(1 << 30)), key_bits=key_bits)
+    if kind == "few":          # a handful of distinct values
+        vals = datagen.gen_u64(7, seed=int(rng.integers(1 << 30)), key_bits=key_bits)
+        k = vals[k % np.uint64(7)]
+    elif kind == "sorted":
+        k = np.sort(k)
+    elif kind == "reverse":
+        k = np.sort(k)[::-1].copy()
+    elif kind == "lowbits":    # only the low 20 bits vary
+        k = (k & np.uint64((1 << min(20, key_bits)) - 1)) | (np.uint64(0xABCDEF) << np.uint64(max(0, key_bits - 24))
+                                                             if key_bits > 24 else np.uint64(0))
+        if key_bits < 64:
+            k &= np.uint64((1 << key_bits) - 1)
+    elif kind == "bincap":     # top-16 bins right at the local-sort capacity (8,704)
+        top = (np.arange(n, dtype=np.uint64) // np.uint64(8704)) << np.uint64(key_bits - 16)
+        k = top | (k & np.uint64((1 << (key_bits - 16)) - 1))
+        k = k[rng.permutation(n)]
+    return k
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_pairs_and_keys(cuda, case):
+    """Random sizes around the MSD threshold, key widths and adversarial shapes
+    (few distinct values, sorted, reverse, low-entropy, bins exactly at the
+    local-sort capacity) through all three wide entry points; oracle, bit-exact."""
+    rng = np.random.default_rng(1000 + case)
+    kinds = ["uniform", "few", "sorted", "reverse", "lowbits", "bincap"]
+    kind = kinds[case % len(kinds)]
+    key_bits = int(rng.choice([32, 37, 48, 56, 64])) if kind != "bincap" else 64
+    n = int(rng.integers((1 << 22) - 1000, 3 * (1 << 21))) if case % 2 == 0 else int(rng.integers(1, 300_000))
+    k = _fuzz_keys(rng, n, key_bits, kind)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda), key_bits=key_bits)
+    ek, ev = oracle.sort_pairs_u64_u32(k, v, key_bits)
+    np.testing.assert_array_equal(to_host(ko), ek, err_msg=f"{kind} n={n} kb={key_bits}")
+    np.testing.assert_array_equal(to_host(vo), ev, err_msg=f"{kind} n={n} kb={key_bits}")
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda), key_bits=key_bits)), ek)
+    if key_bits <= 32:
+        k32 = k.astype(np.uint32)
+        np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k32, cuda), key_bits=key_bits)),
+                                      oracle.sort_keys_u32(k32, key_bits))
