@@ -311,14 +311,12 @@ def run_fs(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        hist = torch.empty(65536, dtype=torch.int64, device=dev)
-        prefix = torch.empty(65537, dtype=torch.int64, device=dev)
+        prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
         htemp = torch.empty(L.fs_histogram_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
-        stemp = torch.empty(L.fs_exclusive_scan_u64_temp_bytes(65536), dtype=torch.uint8, device=dev)
         b0, b1 = (n_total * rank) // world, (n_total * (rank + 1)) // world
     else:
         temp = torch.empty(L.fs_sort_keys_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
-    nev = 4 if world == 1 else 5
+    nev = 4
     # Phase events on every PHASE_EVERY-th timed step (a sample of the timed
     # region); the whole region is bracketed by t_begin / t_end.  Recording
     # events at every boundary of every step adds a few us per step.
@@ -342,20 +340,18 @@ def run_fs(args, rank, world, local_rank):
         else:
             if ev_row is not None:
                 ev_row[0].record(stream)
-            _lib.check(L.fs_histogram_u16(keys.data_ptr(), n, 16, hist.data_ptr(), 0, htemp.data_ptr(),
-                                          htemp.numel(), s), "fs_histogram_u16")
+            _lib.check(L.fs_histogram_prefix_u16(keys.data_ptr(), n, prefix2.data_ptr(), htemp.data_ptr(),
+                                                 htemp.numel(), s), "fs_histogram_prefix_u16")
             if ev_row is not None:
                 ev_row[1].record(stream)
-            dist.all_reduce(hist)  # NCCL, 512 KiB: the global histogram merge across GPUs
+            # NCCL, 513 KiB: the global histogram merge across GPUs, in the
+            # sort's two-level prefix form (linear in the counts: no scan after it)
+            dist.all_reduce(prefix2)
             if ev_row is not None:
                 ev_row[2].record(stream)
-            _lib.check(L.fs_exclusive_scan_u64(hist.data_ptr(), prefix.data_ptr(), 65536, stemp.data_ptr(),
-                                               stemp.numel(), s), "fs_exclusive_scan_u64")
+            _lib.check(L.fs_expand_prefix_u16(prefix2.data_ptr(), b0, b1, out.data_ptr(), s), "fs_expand_prefix_u16")
             if ev_row is not None:
                 ev_row[3].record(stream)
-            _lib.check(L.fs_expand_u16(prefix.data_ptr(), 65536, b0, b1, out.data_ptr(), s), "fs_expand_u16")
-            if ev_row is not None:
-                ev_row[4].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -388,8 +384,8 @@ def run_fs(args, rank, world, local_rank):
         names = {"hist16": phase_ms[1], "expand16": phase_ms[2]}  # phase 0 is empty (no memset)
         scan_ms = phase_ms[1]
     else:
-        names = {"hist16+merge": phase_ms[0], "expand16": phase_ms[3]}
-        scan_ms = phase_ms[2]
+        names = {"hist16+merge+scan": phase_ms[0], "expand16": phase_ms[2]}
+        scan_ms = phase_ms[0]
     dom = max(names, key=names.get)
     dom_ms = names[dom]
     alg_bytes = 2 * (n if world == 1 else (b1 - b0) if dom == "expand16" else n)
@@ -403,7 +399,7 @@ def run_fs(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
         "config": {"workload": workload_text if (n == n_default or args.workload == "c4") else f"{n} uint16 keys per GPU, {dist_name}, seed 0",
                    "keys_per_gpu": n, "keys_total": n_total, "parallelism": f"dp{world}",
-                   "multi_gpu_mode": None if world == 1 else "B (histogram all-reduce + own-range expansion)",
+                   "multi_gpu_mode": None if world == 1 else "B (two-level prefix all-reduce + own-range expansion)",
                    "l2": (f"inputs ({n * 2 / 2**20:.0f} MiB/GPU) larger than L2 (126 MB): no flush between steps" if n * 2 > 126e6
                           else "L2-resident input (c1): launch-bound, no roofline claim")},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -414,9 +410,9 @@ def run_fs(args, rank, world, local_rank):
                        "frac_of_measured_peak": round(whole_bytes / (t_max / args.steps * 1e-3) / 1e9 / peak, 4),
                        "frac_of_8TBps": round(whole_bytes / (t_max / args.steps * 1e-3) / 8e12, 4)},
         "phases_ms": {k: round(v, 5) for k, v in zip(
-            (["prologue", "hist16+merge+scan", "expand16"] if world == 1 else ["hist16+merge", "nccl_allreduce", "scan", "expand16"]),
+            (["prologue", "hist16+merge+scan", "expand16"] if world == 1 else ["hist16+merge+scan", "nccl_allreduce", "expand16"]),
             phase_ms)},
-        "gpu_launches": (2 if world == 1 else 3) * args.steps,
+        "gpu_launches": 2 * args.steps,
         "clocks": clocks.summary(),
         "phase_events": f"recorded on every {PHASE_EVERY}th of the {args.steps} timed steps ({len(events)} steps); "
                         "ms_per_step from events bracketing the whole timed region",
@@ -464,20 +460,16 @@ def e2e(args, L, _lib, keys, n, n_total, rank, world, dev, dist):
     else:
         d_in = torch.empty(n, dtype=torch.uint16, device=dev)
         d_out = torch.empty(n, dtype=torch.uint16, device=dev)
-        hist = torch.empty(65536, dtype=torch.int64, device=dev)
-        prefix = torch.empty(65537, dtype=torch.int64, device=dev)
+        prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
         htemp = torch.empty(L.fs_histogram_u16_temp_bytes(n), dtype=torch.uint8, device=dev)
-        stemp = torch.empty(L.fs_exclusive_scan_u64_temp_bytes(65536), dtype=torch.uint8, device=dev)
         b0, b1 = (n_total * rank) // world, (n_total * (rank + 1)) // world
 
         def one():
             d_in.copy_(host_in, non_blocking=True)
-            _lib.check(L.fs_histogram_u16(d_in.data_ptr(), n, 16, hist.data_ptr(), 0, htemp.data_ptr(),
-                                          htemp.numel(), s), "fs_histogram_u16")
-            dist.all_reduce(hist)
-            _lib.check(L.fs_exclusive_scan_u64(hist.data_ptr(), prefix.data_ptr(), 65536, stemp.data_ptr(),
-                                               stemp.numel(), s), "fs_exclusive_scan_u64")
-            _lib.check(L.fs_expand_u16(prefix.data_ptr(), 65536, b0, b1, d_out.data_ptr(), s), "fs_expand_u16")
+            _lib.check(L.fs_histogram_prefix_u16(d_in.data_ptr(), n, prefix2.data_ptr(), htemp.data_ptr(),
+                                                 htemp.numel(), s), "fs_histogram_prefix_u16")
+            dist.all_reduce(prefix2)
+            _lib.check(L.fs_expand_prefix_u16(prefix2.data_ptr(), b0, b1, d_out.data_ptr(), s), "fs_expand_prefix_u16")
             host_out[:b1 - b0].copy_(d_out[:b1 - b0], non_blocking=True)
         h2d, d2h = 2 * n, 2 * (b1 - b0)
     one()
@@ -498,7 +490,7 @@ def e2e(args, L, _lib, keys, n, n_total, rank, world, dev, dist):
     return {"value": round(n_total * steps / (ms * 1e-3) / 1e9, 4), "unit": "Gkeys/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "api": "fs_sort_keys_u16_host (pinned host buffers, batched copy/compute overlap)" if world == 1
-            else "H2D + fs_histogram_u16 + NCCL all_reduce + fs_exclusive_scan_u64 + fs_expand_u16 + D2H"}
+            else "H2D + fs_histogram_prefix_u16 + NCCL all_reduce + fs_expand_prefix_u16 + D2H"}
 
 
 def verify(out, keys):

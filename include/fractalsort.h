@@ -138,6 +138,20 @@ fs_status fs_sort_pairs_u64_u32(const uint64_t* keys_in, const uint32_t* vals_in
 fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint64_t* hist, int accumulate,
                            void* temp, size_t temp_bytes, fs_stream_t stream);
 
+/* fs_histogram_prefix_u16 / fs_expand_prefix_u16: the sort's own two-level
+ * prefix, exported for the multi-GPU path (SURVEY.md §8(e) Mode B).  prefix2
+ * holds 65,536 + 128 u64: prefix2[v] = #keys < v inside v's 512-bin slice
+ * (slice-local GetIndex, Alg. 3) and prefix2[65536 + s] = the total of slice s.
+ * Both parts are linear in the counts, so the element-wise sum over ranks
+ * (one all-reduce) is the same form for the union of the shards; expansion of
+ * global positions [out_begin, out_end) then needs no scan kernel (the slice
+ * bases are folded into the expansion).  temp as for
+ * fs_histogram_u16; keys 2-byte aligned; the buffers must not overlap. */
+fs_status fs_histogram_prefix_u16(const uint16_t* keys, uint64_t n, uint64_t* prefix2, void* temp, size_t temp_bytes,
+                                  fs_stream_t stream);
+fs_status fs_expand_prefix_u16(const uint64_t* prefix2, uint64_t out_begin, uint64_t out_end, uint16_t* out,
+                               fs_stream_t stream);
+
 /* fs_exclusive_scan_u64: prefix[v] = sum_{u<v} hist[u] for v = 0..nbins, so
  * prefix[nbins] is the total (Alg. 3 GetIndex for every v).
  * hist: nbins u64; prefix: nbins + 1 u64; they must not overlap.  Single-pass

@@ -21,7 +21,7 @@ from ._lib import FractalSortError, check, lib
 __all__ = [
     "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
-    "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
+    "histogram_prefix_u16", "expand_prefix_u16", "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
 ]
 
 _TEMP_ALIGN = 256
@@ -119,6 +119,35 @@ def histogram_u16(keys: torch.Tensor, key_bits: int = 16, hist: torch.Tensor | N
         check(L.fs_histogram_u16(keys.data_ptr(), n, key_bits, hist.data_ptr(), int(bool(accumulate)),
                                  temp.data_ptr(), temp.numel(), _stream(dev)), "fs_histogram_u16")
     return hist
+
+
+def histogram_prefix_u16(keys: torch.Tensor, prefix2: torch.Tensor | None = None) -> torch.Tensor:
+    """The sort's two-level prefix of keys: 65,536 slice-local prefixes + 128 slice totals, int64
+    (fs_histogram_prefix_u16); sums over ranks stay in the same form."""
+    dev = _require_cuda(keys)
+    if keys.dtype != torch.uint16:
+        raise TypeError("histogram_prefix_u16 expects uint16 keys")
+    if prefix2 is None:
+        prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
+    n = keys.numel()
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_histogram_u16_temp_bytes(n), dev)
+        check(L.fs_histogram_prefix_u16(keys.data_ptr(), n, prefix2.data_ptr(), temp.data_ptr(), temp.numel(),
+                                        _stream(dev)), "fs_histogram_prefix_u16")
+    return prefix2
+
+
+def expand_prefix_u16(prefix2: torch.Tensor, out_begin: int, out_end: int, out: torch.Tensor | None = None):
+    """Keys at global sorted positions [out_begin, out_end) from a two-level prefix (fs_expand_prefix_u16)."""
+    dev = _require_cuda(prefix2)
+    n = out_end - out_begin
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint16, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_expand_prefix_u16(prefix2.data_ptr(), out_begin, out_end, out.data_ptr(), _stream(dev)),
+              "fs_expand_prefix_u16")
+    return out
 
 
 def exclusive_scan(hist: torch.Tensor) -> torch.Tensor:

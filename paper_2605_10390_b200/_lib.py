@@ -31,6 +31,8 @@ SIGNATURES = {
     "fs_sort_pairs_u64_u32": (_i32, [_vp, _vp, _vp, _vp, _u64, _i32, _vp, _sz, _vp]),
     "fs_histogram_u16": (_i32, [_vp, _u64, _i32, _vp, _i32, _vp, _sz, _vp]),
     "fs_exclusive_scan_u64": (_i32, [_vp, _vp, _u64, _vp, _sz, _vp]),
+    "fs_histogram_prefix_u16": (_i32, [_vp, _u64, _vp, _vp, _sz, _vp]),
+    "fs_expand_prefix_u16": (_i32, [_vp, _u64, _u64, _vp, _vp]),
     "fs_expand_u16": (_i32, [_vp, _u64, _u64, _u64, _vp, _vp]),
     "fs_send_counts": (_i32, [_vp, _i32, _i32, _u64, _vp, _vp]),
     "fs_sort_keys_u16_host_work_bytes": (_sz, [_u64, _u64]),

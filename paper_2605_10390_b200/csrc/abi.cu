@@ -209,6 +209,47 @@ fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint6
   return finish(s, "fs_histogram_u16");
 }
 
+fs_status fs_histogram_prefix_u16(const uint16_t* keys, uint64_t n, uint64_t* prefix2, void* temp, size_t temp_bytes,
+                                  fs_stream_t stream) {
+  clear_error();
+  if (!prefix2) return fail(FS_ERR_INVALID_ARGUMENT, "prefix2 is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(prefix2, 0, sizeof(uint64_t) * (kHistBins + kHistSlices), s);
+    if (e != cudaSuccess) return cuda_fail(e, "fs_histogram_prefix_u16: memset");
+    return finish(s, "fs_histogram_prefix_u16");
+  }
+  if (!keys || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer with n > 0");
+  if ((uintptr_t)temp & 255) return fail(FS_ERR_INVALID_ARGUMENT, "temp not 256-byte aligned");
+  if ((uintptr_t)keys & 1) return fail(FS_ERR_INVALID_ARGUMENT, "keys not 2-byte aligned");
+  const U16Layout L = u16_layout(n, false);
+  if (temp_bytes < L.total)
+    return fail(FS_ERR_INVALID_ARGUMENT, "temp_bytes %zu < required %zu", temp_bytes, L.total);
+  const size_t pb = sizeof(uint64_t) * (kHistBins + kHistSlices);
+  if (overlaps(temp, L.total, prefix2, pb) || overlaps(temp, L.total, keys, 2 * n) || overlaps(keys, 2 * n, prefix2, pb))
+    return fail(FS_ERR_INVALID_ARGUMENT, "temp, keys and prefix2 must not overlap");
+  char* t = (char*)temp;
+  cudaError_t e = launch_hist16(keys, n, (uint32_t*)(t + L.partials_off), (unsigned long long*)(t + L.spill_off),
+                                nullptr, 0, 0, prefix2, prefix2 + kHistBins, L.grid, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_histogram_prefix_u16");
+  return finish(s, "fs_histogram_prefix_u16");
+}
+
+fs_status fs_expand_prefix_u16(const uint64_t* prefix2, uint64_t out_begin, uint64_t out_end, uint16_t* out,
+                               fs_stream_t stream) {
+  clear_error();
+  if (out_end < out_begin) return fail(FS_ERR_INVALID_ARGUMENT, "out_end < out_begin");
+  if (out_end == out_begin) return FS_OK;
+  if (!prefix2 || !out) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if ((uintptr_t)out & 1) return fail(FS_ERR_INVALID_ARGUMENT, "out not 2-byte aligned");
+  if (overlaps(prefix2, sizeof(uint64_t) * (kHistBins + kHistSlices), out, 2 * (out_end - out_begin)))
+    return fail(FS_ERR_INVALID_ARGUMENT, "prefix2 and out overlap");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_expand16_two_level(prefix2, prefix2 + kHistBins, out_begin, out_end, out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_expand_prefix_u16");
+  return finish(s, "fs_expand_prefix_u16");
+}
+
 fs_status fs_exclusive_scan_u64(const uint64_t* hist, uint64_t* prefix, uint64_t nbins, void* temp,
                                 size_t temp_bytes, fs_stream_t stream) {
   clear_error();

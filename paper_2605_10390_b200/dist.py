@@ -8,9 +8,11 @@ and the exact output partition needs no sampling: rank d owns global sorted
 positions [floor(d*N/G), floor((d+1)*N/G)) (ledger 23).
 
 mode "B" (compressed exchange, the scaling path): the exchanged form of a shard
-    is its 512 KiB histogram.  all_reduce(hist) -> scan -> expand the rank's own
-    output range.  NVLink carries 512 KiB per rank, HBM 4 B/key of the rank's
-    share: near-linear by construction.
+    is its histogram, as the sort's two-level prefix (slice-local prefixes +
+    slice totals, linear in the counts).  all_reduce of those 65,664 counters
+    -> expand the rank's own output range (no scan kernel: the slice bases are
+    folded into the expansion).  NVLink carries 513 KiB per rank, HBM 4 B/key of
+    the rank's share: near-linear by construction.
 mode "A" (payload exchange by key range, the literal c4 reading): local sort of
     the shard, all_gather of the histograms, exact send counts (fs_send_counts:
     lower rank first for equal keys), all_to_all_single of the key
@@ -38,6 +40,14 @@ class CudaOps:
     def histogram_u16(self, keys):
         from . import histogram_u16
         return histogram_u16(keys)                  # int64[65536]
+
+    def histogram_prefix_u16(self, keys):
+        from . import histogram_prefix_u16
+        return histogram_prefix_u16(keys)           # int64[65536 + 128]
+
+    def expand_prefix_u16(self, prefix2, begin, end):
+        from . import expand_prefix_u16
+        return expand_prefix_u16(prefix2, begin, end)
 
     def exclusive_scan(self, hist):
         from . import exclusive_scan
@@ -115,12 +125,11 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
     rank = dist.get_rank(group)
     dev = shard.device
     if mode == "B":
-        hist = ops.histogram_u16(shard)
-        dist.all_reduce(hist, group=group)
-        prefix = ops.exclusive_scan(hist)
-        n_total = int(prefix[-1].item())
+        prefix2 = ops.histogram_prefix_u16(shard)
+        dist.all_reduce(prefix2, group=group)
+        n_total = int(prefix2[65536:].sum().item())
         begin, end = output_range(rank, world, n_total)
-        return ops.expand_u16(prefix, begin, end), (begin, end)
+        return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)
     if mode == "A":
         hist = ops.histogram_u16(shard)
         gathered = [torch.empty_like(hist) for _ in range(world)]

@@ -26,6 +26,21 @@ class OracleOps:
         import oracle
         return torch.from_numpy(oracle.histogram_u16(keys.numpy()).astype(np.int64))
 
+    def histogram_prefix_u16(self, keys):
+        """Two-level form: slice-local exclusive prefixes (512-bin slices) + slice totals."""
+        import oracle
+        P = oracle.exclusive_scan(oracle.histogram_u16(keys.numpy())).astype(np.int64)
+        L = P[:65536] - np.repeat(P[0:65536:512], 512)
+        tot = P[512:65537:512] - P[0:65536:512]
+        return torch.from_numpy(np.concatenate([L, tot]).astype(np.int64))
+
+    def expand_prefix_u16(self, prefix2, begin, end):
+        import oracle
+        p2 = prefix2.numpy().astype(np.int64)
+        base = np.concatenate([[0], np.cumsum(p2[65536:])])[:128]
+        P = np.concatenate([p2[:65536] + np.repeat(base, 512), [p2[65536:].sum()]]).astype(np.uint64)
+        return torch.from_numpy(oracle.reconstruct_counts_u16(np.diff(P), begin, end))
+
     def exclusive_scan(self, hist):
         import oracle
         return torch.from_numpy(oracle.exclusive_scan(hist.numpy().astype(np.uint64)).astype(np.int64))

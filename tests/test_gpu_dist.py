@@ -81,3 +81,16 @@ def test_dist_pairs_single_rank(cuda, nccl_group):
     assert (b, e) == (0, k.size)
     np.testing.assert_array_equal(ko.cpu().numpy(), ek)
     np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+
+
+@pytest.mark.parametrize("dist_name", ["uniform", "zipf", "const"])
+def test_two_level_prefix_sum_over_ranks(cuda, dist_name):
+    """fs_histogram_prefix_u16 of shards summed element-wise (what the all-reduce
+    does) and expanded per output range = the oracle sort of the union."""
+    import paper_2605_10390_b200 as fs
+    keys = datagen.gen_u16(dist_name, 3_000_017, seed=7)
+    cuts = [0, 700_001, 2_100_000, keys.size]
+    p2 = sum(fs.histogram_prefix_u16(torch.from_numpy(keys[a:b].copy()).to(cuda)) for a, b in zip(cuts, cuts[1:]))
+    want = oracle.sort_u16(keys)
+    for a, b in [(0, keys.size), (0, 1), (12345, 1_234_567), (keys.size - 9, keys.size)]:
+        np.testing.assert_array_equal(fs.expand_prefix_u16(p2, a, b).cpu().numpy(), want[a:b])
