@@ -411,7 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
 }  // namespace
 
 int hist16_grid(uint64_t n) {
-  const uint64_t want = (n + 65535) / 65536;  // keep >= 64K keys per CTA: the flush is 128 KB
+#ifndef FS_HIST_KEYS_PER_CTA
+#define FS_HIST_KEYS_PER_CTA 65536
+#endif
+  // keep >= FS_HIST_KEYS_PER_CTA keys per CTA: every CTA zeroes and flushes 128 KB
+  const uint64_t want = (n + FS_HIST_KEYS_PER_CTA - 1) / FS_HIST_KEYS_PER_CTA;
   const uint64_t sms = (uint64_t)device_info().sm_count;
   uint64_t g = want < sms ? want : sms;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence in one gpurun call: GPU tests, smoke, bench lines for every
 # config, ncu launch lists, and ncu --set full captures of the top kernels.
-O=gpurun_out/round
+O=gpurun_out/${ROUND_DIR:-round}
 mkdir -p $O
 make -j8 all > $O/build.log 2>&1 || { tail -30 $O/build.log; exit 1; }
 nvidia-smi > $O/nvidia-smi.txt 2>&1
@@ -10,6 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err; tail -c 400 $O/bench_c2.json
 for w in c1 c3a c3b c3c c3d; do timeout 600 python bench.py --workload $w --steps 50 --warmup 5 --no-e2e --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
 timeout 900 python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err; tail -c 300 $O/bench_c5.json
+timeout 900 python bench.py --workload c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c4_1gpu.json 2> $O/bench_c4.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 NB="--no-e2e --no-cpu-baseline --no-verify"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 5 --warmup 3 $NB > $O/ncu_launch_c2.log 2>&1

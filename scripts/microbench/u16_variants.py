@@ -6,8 +6,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 import datagen
 
-n = 1 << 28
 dist = sys.argv[1] if len(sys.argv) > 1 else "uniform"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 28
 dev = torch.device("cuda", 0)
 s = torch.cuda.current_stream().cuda_stream
 k = torch.empty(n, dtype=torch.uint16, device=dev)
