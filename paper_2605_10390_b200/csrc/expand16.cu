@@ -37,7 +37,6 @@ constexpr int kThreads = 256;
 #define FS_EXPAND_VPT 16
 #endif
 constexpr int kVecPerThread = FS_EXPAND_VPT;                       // max 16-byte vectors per thread
-constexpr uint64_t kTile = (uint64_t)kThreads * kVecPerThread * 8;  // 32,768 keys = 64 KB of output (max)
 constexpr int kSliceCap = 4096;                                    // staged P entries
 constexpr int kSliceShift = 9;                                     // two-level: 512-bin slices
 constexpr int kNumSlices = 65536 >> kSliceShift;                   // 128

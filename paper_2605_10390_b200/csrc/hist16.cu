@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   const uint64_t nstatic = ngroups - ngroups / FS_HIST_DYN_DIV;
   bool agg = false;
   uint32_t phase = 0;
-  // v[u] = p[u * stride]; the whole warp calls this together.
+  // the whole warp calls this together (warp votes inside)
   auto process_v = [&](uint4 (&v)[kUnroll]) {
     if (agg || phase == 0) {
       bool runs = false;
@@ -228,12 +228,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
         for (int u = 0; u < kUnroll; ++u) recheck8(sh, v[u], a.spill);
       }
     }
-  };
-  auto process = [&](const uint4* p, uint32_t stride) {
-    uint4 v[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream_v4(p + u * stride);
-    process_v(v);
   };
   // Static groups, software-pipelined: group g + G is loaded before group g's
   // atomics, so a warp never waits on HBM between its atomic bursts

@@ -28,7 +28,6 @@ __global__ void __launch_bounds__(kThreads)
     k_send_counts(const uint64_t* __restrict__ C, int G, int g, uint64_t nbins, uint64_t* __restrict__ send) {
   __shared__ unsigned long long acc[kMaxRanks];
   __shared__ unsigned long long warp_tot[kThreads / 32];
-  __shared__ unsigned long long total_sh;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   for (int d = tid; d < G; d += kThreads) acc[d] = 0;
 
@@ -49,7 +48,6 @@ __global__ void __launch_bounds__(kThreads)
     N += warp_tot[w];
   }
   base += inc - mine;
-  if (tid == 0) total_sh = N;
   __syncthreads();
 
   unsigned long long Pv = base;
