@@ -101,14 +101,21 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
                            size_t temp_bytes, fs_stream_t stream);
 
 /* ----------------------------------------------------------------------------
- * fs_sort_keys_u32 / fs_sort_keys_u64 — keys-only ascending sort of wider keys:
- * stable LSD radix ("histogram, prefix sum and stable scatter phases",
- * PAPER.md:52 §II) with 8-bit digits and one compressed histogram per digit,
- * all digit histograms computed in one read pass (config c5's "multi-digit
- * precision scaling with compressed histograms per digit", ledger 25).
- * ceil(key_bits / 8) scatter passes; a digit whose histogram has one non-empty
- * bin is skipped.  keys_in and keys_out must not overlap.  key_bits: 0 or
- * 1..32 (u32), 0 or 1..64 (u64).
+ * fs_sort_keys_u32 / fs_sort_keys_u64 — keys-only ascending sort of wider keys.
+ * Two schemes with the same (unique) result:
+ *  - trie-binned MSD (NEXT-1; n >= 2^22 and key_bits >= 32): one read builds the
+ *    leaf level of a 16-level compressed trie over the top 16 key bits; its
+ *    level-8 and level-16 counters bound two stable 8-bit MSD scatters; every
+ *    16-bit bin is then sorted by its remaining bits in shared memory (Alg. 5's
+ *    bins and per-bin sort).  Taken when every bin
+ *    holds <= 8,704 keys — decided on the device, no host synchronisation;
+ *  - otherwise stable LSD radix ("histogram, prefix sum and stable scatter
+ *    phases", §II) with 8-bit digits and one compressed histogram
+ *    per digit, all digit histograms in one read pass (config c5's "multi-digit
+ *    precision scaling with compressed histograms per digit", ledger 25); a
+ *    digit whose histogram has one non-empty bin is skipped.
+ * keys_in and keys_out must not overlap.  key_bits: 0 or 1..32 (u32), 0 or
+ * 1..64 (u64).
  * ------------------------------------------------------------------------- */
 fs_status fs_sort_keys_u32(const uint32_t* keys_in, uint32_t* keys_out, uint64_t n, int key_bits, void* temp,
                            size_t temp_bytes, fs_stream_t stream);
@@ -119,7 +126,7 @@ fs_status fs_sort_keys_u64(const uint64_t* keys_in, uint64_t* keys_out, uint64_t
  * fs_sort_pairs_u64_u32 — STABLE ascending sort of (u64 key, u32 value) pairs
  * by key (config c5).  Equal keys keep their input order, so with
  * vals_in[i] = i the output values are Alg. 5's index array I.
- * Same LSD scheme as fs_sort_keys_u64; keys and values move together.
+ * Same schemes as fs_sort_keys_u64; keys and values move together.
  * No input buffer may overlap an output buffer.
  * ------------------------------------------------------------------------- */
 fs_status fs_sort_pairs_u64_u32(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
@@ -287,7 +294,12 @@ fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out,
  *   fs_sort_keys_u16:  [0] start, [1] after zeroing the temp counters, [2] after
  *                      the histogram+merge+scan kernel, [3] after the expansion
  *                      kernel;
- *   wide sorts:        [0] start, [1] after the digit histograms + plan,
+ *   wide sorts, MSD planned (n >= 2^22, key_bits >= 32): [0] start, [1] after
+ *                      the trie histogram + scan + plan, [2] level-1 scatter,
+ *                      [3] level-2 scatter, [4] per-bin sort, [5] after the LSD
+ *                      digit histograms (they return at once when MSD ran),
+ *                      [6 + p] after LSD pass p, last after the identity copy;
+ *   wide sorts, LSD only: [0] start, [1] after the digit histograms + plan,
  *                      [2 + p] after scatter pass p (passes ceil(key_bits/8)),
  *                      last after the identity copy check.
  * The library does not own or destroy the events.  Returns FS_OK.

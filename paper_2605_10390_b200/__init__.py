@@ -54,7 +54,9 @@ def sort_keys(keys: torch.Tensor, key_bits: int = 0, out: torch.Tensor | None = 
     """Ascending keys-only sort of a 1-D uint16/uint32/uint64 CUDA tensor.
 
     uint16 -> fs_sort_keys_u16 (histogram, scan, count-expansion; out may be keys);
-    uint32/uint64 -> fs_sort_keys_u32/u64 (LSD with one compressed histogram per digit).
+    uint32/uint64 -> fs_sort_keys_u32/u64 (trie-binned MSD with a per-bin shared-memory sort
+    for n >= 2^22 and key_bits >= 32, decided bin by bin on the device; else LSD with one
+    compressed histogram per 8-bit digit).
     """
     dev = _require_cuda(keys)
     n = keys.numel()
