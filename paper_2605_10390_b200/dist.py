@@ -84,20 +84,24 @@ class CudaOps:
 class PeerBuffers:
     """Every rank's output buffer, mapped into every rank (CUDA IPC through
     torch's tensor sharing; peer access over NVLink is enabled by the mapping).
-    Buffers hold ceil(N / G) keys (every rank's range fits) and are reallocated,
-    collectively, only when a larger N arrives."""
+    Buffers hold ceil(N / G) elements (every rank's range fits) and are
+    reallocated, collectively, only when a larger N arrives.  dtype: uint16
+    keys (mode "P"), uint64 keys / uint32 values (pairs, mode "P")."""
 
-    def __init__(self, device, group=None):
-        self.device, self.group, self.capacity, self.views = device, group, 0, None
+    _STORAGE = {torch.uint16: torch.int16, torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+    def __init__(self, device, group=None, dtype=torch.uint16):
+        self.device, self.group, self.dtype, self.capacity, self.views = device, group, dtype, 0, None
 
     def buffers(self, per_rank: int):
         if per_rank > self.capacity:
             from torch.multiprocessing.reductions import reduce_tensor
             world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
-            own = torch.empty(max(per_rank, 1), dtype=torch.uint16, device=self.device)
+            own = torch.empty(max(per_rank, 1), dtype=self._STORAGE[self.dtype], device=self.device)
             handles = [None] * world
             dist.all_gather_object(handles, reduce_tensor(own) if world > 1 else None, group=self.group)
-            self.views = [own if r == rank else handles[r][0](*handles[r][1]) for r in range(world)]
+            views = [own if r == rank else handles[r][0](*handles[r][1]) for r in range(world)]
+            self.views = [v.view(self.dtype) for v in views]
             self.capacity = per_rank
         return self.views
 
@@ -174,7 +178,8 @@ def _u64_tensor(values, device):
     return torch.from_numpy(np.array(values, dtype=np.uint64).view(np.int64)).to(device).view(torch.uint64)
 
 
-def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=None, key_bits: int = 64):
+def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=None, key_bits: int = 64,
+                       mode: str = "A", peers=None):
     """Stable sort of the (u64 key, u32 value) pairs of all ranks (SURVEY.md §8(e)
     Mode A for pairs): the ranks' shards are contiguous slices of the input in
     rank order, so the global stable order breaks key ties by (rank, local
@@ -185,8 +190,12 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
        the key K_d of the element at global position s_d is found by bisection
        over the key space, each step one fs_bound_u64 (rank counts) and one
        all_reduce; ties at K_d are split by source rank (ledger 13, 23);
-    3. all_to_all of keys and values by those cuts (the payload exchange);
+    3. the payload exchange by those cuts: mode "A" all_to_all of keys and
+       values (NCCL); mode "P" (NEXT-2) every rank stores its slices straight
+       into the owners' receive buffers, mapped with CUDA IPC (peer copies over
+       NVLink, no staging), at offsets from one all_gather of the send counts;
     4. stable local sort of what arrived (runs arrive in source-rank order).
+    ``peers``: (keys, values) PeerBuffers to reuse across calls (mode "P").
     """
     if keys.dtype != torch.uint64 or vals.dtype != torch.uint32 or keys.numel() != vals.numel():
         raise TypeError("uint64 keys and uint32 values of equal length expected")
@@ -234,6 +243,26 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
     cuts.append(n_local)
     send = [cuts[d + 1] - cuts[d] for d in range(world)]
     send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    if mode == "P":
+        gathered_send = [torch.empty_like(send_t) for _ in range(world)]
+        dist.all_gather(gathered_send, send_t, group=group)
+        all_send = torch.stack(gathered_send).cpu().tolist()       # [source][dest]
+        assert sum(all_send[r][rank] for r in range(world)) == end - begin
+        if peers is None:
+            peers = (PeerBuffers(dev, group, torch.uint64), PeerBuffers(dev, group, torch.uint32))
+        cap = -(-N // world)
+        pk, pv = peers[0].buffers(cap), peers[1].buffers(cap)
+        for d in range(world):
+            if send[d]:
+                off = sum(all_send[r][d] for r in range(rank))       # lower ranks first (stable)
+                pk[d][off:off + send[d]].copy_(ks[cuts[d]:cuts[d + 1]], non_blocking=True)
+                pv[d][off:off + send[d]].copy_(vs[cuts[d]:cuts[d + 1]], non_blocking=True)
+        ops.synchronize(dev)
+        dist.barrier(group=group)                                   # every producer has finished writing
+        rk, rv = pk[rank][:end - begin], pv[rank][:end - begin]
+        if rk.numel():
+            rk, rv = ops.sort_pairs(rk, rv)
+        return (rk, rv), (begin, end)
     recv_t = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.tolist()]

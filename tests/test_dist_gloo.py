@@ -176,7 +176,8 @@ def test_output_range_helper():
     assert sorted(e - b for b, e in ranges) == [4, 4, 4, 5]
 
 
-PAIR_CASES = [("uniform", False), ("ties8", True), ("const", False), ("ties3", True)]
+PAIR_CASES = [("uniform", False, "A"), ("ties8", True, "A"), ("const", False, "A"), ("ties3", True, "A"),
+              ("uniform", True, "P"), ("ties8", False, "P"), ("const", True, "P")]
 N_PAIRS = 20_011
 
 
@@ -192,18 +193,20 @@ def pair_input(kind):
     return k, datagen.iota_u32(N_PAIRS)
 
 
-def pair_worker(rank, world, port, outdir):
+def pair_worker(rank, world, port, outdir, peer_bufs):
     sys.path.insert(0, ROOT)
     from paper_2605_10390_b200 import dist as fsdist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        for ci, (kind, uneven) in enumerate(PAIR_CASES):
+        for ci, (kind, uneven, mode) in enumerate(PAIR_CASES):
             b, e = shard_bounds(N_PAIRS, world, rank, uneven)
             k, v = pair_input(kind)
+            peers = (SharedPeers(peer_bufs[ci][0]), SharedPeers(peer_bufs[ci][1])) if mode == "P" else None
             (ok, ov), (ob, oe) = fsdist.sort_pairs_u64_u32(torch.from_numpy(k[b:e].copy()),
-                                                           torch.from_numpy(v[b:e].copy()), ops=OracleOps())
+                                                           torch.from_numpy(v[b:e].copy()), ops=OracleOps(),
+                                                           mode=mode, peers=peers)
             np.save(os.path.join(outdir, f"pk_{ci}_{rank}.npy"), ok.numpy())
             np.save(os.path.join(outdir, f"pv_{ci}_{rank}.npy"), ov.numpy())
             np.save(os.path.join(outdir, f"pr_{ci}_{rank}.npy"), np.array([ob, oe], dtype=np.int64))
@@ -213,18 +216,22 @@ def pair_worker(rank, world, port, outdir):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_distributed_pairs_match_oracle(tmp_path, world):
-    """Mode A for pairs: exact splitters by bisection + tie split by source rank,
-    all_to_all, stable local re-sort.  The concatenated slices equal the oracle's
+    """Pairs, modes A (all_to_all) and P (stores into the owners' buffers): exact
+    splitters by bisection + tie split by source rank, exchange, stable local re-sort.  The concatenated slices equal the oracle's
     stable sort of the whole input (values = arrival indices: stability checked)."""
     import oracle
-    mp.start_processes(pair_worker, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True,
+    cap = -(-N_PAIRS // world)
+    peer_bufs = [([torch.zeros(cap, dtype=torch.int64).view(torch.uint64).share_memory_() for _ in range(world)],
+                  [torch.zeros(cap, dtype=torch.int32).view(torch.uint32).share_memory_() for _ in range(world)])
+                 for _ in PAIR_CASES]
+    mp.start_processes(pair_worker, args=(world, free_port(), str(tmp_path), peer_bufs), nprocs=world, join=True,
                        start_method="spawn")
-    for ci, (kind, uneven) in enumerate(PAIR_CASES):
+    for ci, (kind, uneven, mode) in enumerate(PAIR_CASES):
         ks = [np.load(tmp_path / f"pk_{ci}_{r}.npy") for r in range(world)]
         vs = [np.load(tmp_path / f"pv_{ci}_{r}.npy") for r in range(world)]
         ranges = [tuple(np.load(tmp_path / f"pr_{ci}_{r}.npy")) for r in range(world)]
         assert ranges == [((N_PAIRS * d) // world, (N_PAIRS * (d + 1)) // world) for d in range(world)]
         k, v = pair_input(kind)
         ek, ev = oracle.sort_pairs_u64_u32(k, v)
-        np.testing.assert_array_equal(np.concatenate(ks), ek, err_msg=f"{kind} world={world}")
-        np.testing.assert_array_equal(np.concatenate(vs), ev, err_msg=f"{kind} world={world}")
+        np.testing.assert_array_equal(np.concatenate(ks), ek, err_msg=f"{kind} {mode} world={world}")
+        np.testing.assert_array_equal(np.concatenate(vs), ev, err_msg=f"{kind} {mode} world={world}")

@@ -73,10 +73,12 @@ def test_bound_u64_matches_searchsorted(cuda, n):
         np.testing.assert_array_equal(got, np.searchsorted(k, q, side=side).astype(np.int64))
 
 
-def test_dist_pairs_single_rank(cuda, nccl_group):
+@pytest.mark.parametrize("mode", ["A", "P"])
+def test_dist_pairs_single_rank(cuda, nccl_group, mode):
     k = datagen.gen_u64(500_001, seed=5) & np.uint64(0xFF)
     v = datagen.iota_u32(500_001)
-    (ko, vo), (b, e) = fsdist.sort_pairs_u64_u32(torch.from_numpy(k).to(cuda), torch.from_numpy(v).to(cuda))
+    (ko, vo), (b, e) = fsdist.sort_pairs_u64_u32(torch.from_numpy(k).to(cuda), torch.from_numpy(v).to(cuda),
+                                                 mode=mode)
     ek, ev = oracle.sort_pairs_u64_u32(k, v)
     assert (b, e) == (0, k.size)
     np.testing.assert_array_equal(ko.cpu().numpy(), ek)
