@@ -215,3 +215,18 @@ def test_fuzz_pairs_and_keys(cuda, case):
         k32 = k.astype(np.uint32)
         np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k32, cuda), key_bits=key_bits)),
                                       oracle.sort_keys_u32(k32, key_bits))
+
+
+def test_msd_level2_linear_order(cuda):
+    """A first-level bucket holding 30% of the keys (bins still fit the local
+    sort): 256 x (its tiles) exceeds the status rows, so level 2 runs its tiles in
+    linear order with segment-start lookbacks instead of interleaved tickets."""
+    n = (1 << 22) + 5
+    k = datagen.gen_u64(n, seed=77)
+    hot = datagen.gen_u64(n, seed=78) % np.uint64(10) < np.uint64(3)
+    k[hot] = (k[hot] & np.uint64((1 << 56) - 1)) | np.uint64(0x42 << 56)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
