@@ -87,6 +87,10 @@ constexpr int kMaxPasses = 8;
 #define FS_SCATTER_ITEMS 16
 #define FS_SCATTER_MINB 2
 #endif
+#ifndef FS_SCATTER_STORE_UNROLL
+#define FS_SCATTER_STORE_UNROLL 1
+#endif
+constexpr int kStoreUnroll = FS_SCATTER_STORE_UNROLL;
 constexpr int kSThreads = FS_SCATTER_THREADS;
 constexpr int kSWarps = kSThreads / 32;
 constexpr int kSItems = FS_SCATTER_ITEMS;
@@ -744,6 +748,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
 
     FS_PH(4);  // 4: lookback + barrier
     // ---- scatter: consecutive positions of one digit go to consecutive addresses
+#pragma unroll kStoreUnroll
     for (uint32_t j = tid; j < len; j += kSThreads) {
       const K k = kbuf[j];
       const uint64_t dst = sm.gofs[digit_of(k, shift)] + j;
