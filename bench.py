@@ -214,9 +214,9 @@ def run_fs_pairs(args, dev):
     temp = torch.empty(L.fs_sort_pairs_u64_u32_temp_bytes(n, 64), dtype=torch.uint8, device=dev)
     # phase events (include/fractalsort.h): MSD-planned sorts record [0] start,
     # [1] trie histogram + scan + plan, [2] level-1 scatter, [3] level-2 scatter,
-    # [4] per-bin local sort, [5..14] the LSD fallback kernels (they return at
-    # once when the MSD path ran).
-    nev = 15
+    # [4] per-bin local sort, [5] recursion into oversize bins, [6..15] the LSD
+    # kernels (they return at once when the MSD path ran).
+    nev = 16
     steps = args.steps
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(steps)]
     for row in events:
@@ -241,12 +241,12 @@ def run_fs_pairs(args, dev):
         torch.cuda.synchronize()
     total_ms = events[0][0].elapsed_time(events[-1][nev - 1])
     phase = [statistics.mean(r[i].elapsed_time(r[i + 1]) for r in events) for i in range(nev - 1)]
-    names = ["trie_hist+scan+plan", "msd_level1_scatter", "msd_level2_scatter", "local_sort",
+    names = ["trie_hist+scan+plan", "msd_level1_scatter", "msd_level2_scatter", "local_sort", "msd_recursion",
              "lsd_digit_hist+plan"] + [f"lsd_pass{i}" for i in range(8)] + ["lsd_identity_copy"]
-    lsd_ms = sum(phase[4:])
+    lsd_ms = sum(phase[5:])
     path = "msd" if phase[3] > lsd_ms else "lsd-fallback"
     # dominant kernel: each MSD pass reads and writes 8 B key + 4 B value per pair
-    cand = [1, 2, 3] if path == "msd" else list(range(5, 13))
+    cand = [1, 2, 3] if path == "msd" else list(range(6, 14))
     dom = max(cand, key=lambda i: phase[i])
     peak, peak_src = measured_peak_gbs()
     alg = 24 * n
@@ -269,7 +269,7 @@ def run_fs_pairs(args, dev):
                        "method_GBps": round(method_b / (t_step * 1e-3) / 1e9, 1),
                        "frac_method_of_measured_peak": round(method_b / (t_step * 1e-3) / 1e9 / peak, 4)},
         "phases_ms": {nm: round(x, 4) for nm, x in zip(names, phase)},
-        "gpu_launches": (6 + 2 + 8 + 1) * steps,
+        "gpu_launches": 21 * steps,  # MSD: 10 kernels (hist, scan, plan, 2 vseg, 2 scatters, local, recursion, items); LSD: 11 (return at once)
         "clocks": clocks.summary(),
     }
     if not args.no_verify:

@@ -296,9 +296,11 @@ fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out,
  *                      kernel;
  *   wide sorts, MSD planned (n >= 2^22, key_bits >= 32): [0] start, [1] after
  *                      the trie histogram + scan + plan, [2] level-1 scatter,
- *                      [3] level-2 scatter, [4] per-bin sort, [5] after the LSD
- *                      digit histograms (they return at once when MSD ran),
- *                      [6 + p] after LSD pass p, last after the identity copy;
+ *                      [3] level-2 scatter, [4] per-bin sort, [5] recursion
+ *                      into the bins above the local-sort capacity (returns at
+ *                      once if there are none), [6] after the LSD digit
+ *                      histograms (they return at once when MSD ran), [7 + p]
+ *                      after LSD pass p, last after the identity copy;
  *   wide sorts, LSD only: [0] start, [1] after the digit histograms + plan,
  *                      [2 + p] after scatter pass p (passes ceil(key_bits/8)),
  *                      last after the identity copy check.

@@ -38,6 +38,8 @@
 // [flag:2 | pass tag:6 | count:56], reordered through shared memory, offset by a
 // decoupled lookback (one thread per digit, 8 predecessors per round, never
 // crossing a segment start) and written with consecutive addresses per digit.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -138,6 +140,69 @@ struct MsdPlan {
   uint32_t seg_tile0[kSegs + 1];
   uint64_t seg_begin[kSegs + 1];
 };
+
+// ---- recursion into oversize bins (wide_heavy.cuh)
+constexpr uint32_t kHeavyChunkKeys = 65536;  // target keys per chunk
+constexpr uint32_t kHeavyMaxChunks = 1184;   // chunks per segment (bounds phase C's serial loops)
+constexpr int kHeavyThreads = 256;           // = kRadix: thread d owns digit d
+constexpr int kHeavyItems = 16;
+constexpr int kHeavyTile = kHeavyThreads * kHeavyItems;
+constexpr int kHeavyWarps = kHeavyThreads / 32;
+constexpr int kHeavyMaxLevels = 6;           // (64 - 16) / 8
+
+struct HeavySeg {
+  uint64_t begin, count;
+  uint32_t c0, nc;  // chunks [c0, c0 + nc) of the current level
+  uint32_t buf;     // 0: the keys lie in the output, 1: in the temporary buffer
+  uint32_t skip;    // every key has the same digit: not moved at this level
+};
+
+struct HeavyItem {
+  uint64_t begin, count;
+  uint32_t R;    // keys lie in [top, top + 2^R), top = first key with its low `sh` bits cleared;
+                 // sorted by key - top (0: already in order, copy only)
+  uint16_t sh;
+  uint16_t buf;  // where the keys lie
+};
+constexpr uint64_t kHeavyCopyPiece = 1ull << 20;  // copy items are emitted in pieces of this many keys
+
+struct HeavyCtl {
+  uint32_t nseg[2];                     // segments of the level with this parity
+  uint32_t nchunks[kHeavyMaxLevels];
+  uint32_t ticket[kHeavyMaxLevels];
+  uint32_t nitems;
+};
+
+struct HeavyCaps {
+  uint64_t segs, chunks, items;
+};
+
+HeavyCaps heavy_caps(uint64_t n) {
+  HeavyCaps c;
+  c.segs = n / (kLocalCap + 1) + 1;
+  c.chunks = n / kHeavyChunkKeys + c.segs + 1;
+  c.items = (uint64_t)kHeavyMaxLevels * (2 * (n / kLocalCap) + 2 * c.segs + 2 + n / kHeavyCopyPiece + c.segs);
+  return c;
+}
+
+template <typename K>
+struct HeavyArgs {
+  K* kout;
+  uint32_t* vout;
+  K* kalt;
+  uint32_t* valt;
+  int kb;      // key bits
+  int levels;  // ceil((kb - 16) / 8)
+  HeavyCtl* ctl;
+  HeavySeg* seg0;  // segments of even levels
+  HeavySeg* seg1;  // of odd levels
+  uint32_t* chunk_seg;
+  uint32_t* chist;      // [chunk][256]
+  uint64_t* cbase;      // [chunk][256]
+  HeavyItem* items;
+  const MsdPlan* msd;
+};
+
 
 // Stable warp multisplit on an 8-bit digit: the lanes of `valid` holding the
 // same digit as this lane.  Written in PTX so each bit costs setp + vote + selp
@@ -332,24 +397,30 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// MSD plan: whether every 16-bit bin fits the local sort, and the tiles of the
-// level-2 pass (segments = first-level buckets, bounds from P16).
+// MSD plan: the tiles of the level-2 pass (segments = first-level buckets,
+// bounds from P16), and the first level of the recursion: every 16-bit bin
+// above the local-sort capacity becomes a heavy segment.  If one bin holds all
+// the keys (a common 16-bit prefix: the MSD levels would move everything for
+// nothing) the LSD path runs instead, skipping its uniform digits.
 __global__ void __launch_bounds__(kSegs)
-    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint32_t status_cap,
-               MsdPlan* __restrict__ plan) {
+    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
+               MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg) {
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
-  __shared__ int too_big;
+  __shared__ int one_bin;
   const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
   if (s == 0) {
-    too_big = 0;
+    one_bin = 0;
     rmax = 0;
   }
   __syncthreads();
-  uint64_t mx = 0;  // largest bin: coalesced, 16 loads in flight per thread
 #pragma unroll 16
-  for (int j = 0; j < kHistBins / kSegs; ++j) mx = max(mx, (uint64_t)__ldg(H16 + j * kSegs + s));
-  if (mx > (uint64_t)kLocalCap) too_big = 1;
+  for (int j = 0; j < kHistBins / kSegs; ++j) {  // coalesced, 16 loads in flight per thread
+    const uint32_t v = j * kSegs + s;
+    const uint64_t c = __ldg(H16 + v);
+    if (c == n) one_bin = 1;
+    if (c > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{P16[v], c, 0, 0, 0, 0};
+  }
   const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
   const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
   atomicMax(&rmax, tiles);
@@ -371,7 +442,7 @@ __global__ void __launch_bounds__(kSegs)
   }
   __syncthreads();
   if (s == 0) {
-    plan->use_msd = too_big ? 0u : 1u;
+    plan->use_msd = one_bin ? 0u : 1u;
     plan->l2_rmax = rmax;
     // Interleaved tickets keep every segment's lookback one tile deep; worth it
     // unless the segments are so uneven that most tickets would be holes.
@@ -777,17 +848,6 @@ __global__ void k_copy_if_identity(const K* __restrict__ kin, const uint32_t* __
 
 // ================================================================ local sort
 // One CTA per 16-bit bin b = [P16[b], P16[b+1]) of the output (in place): the
-// per-bin sort of Alg. 5 ("sort_bin") by the remaining
-// R = key_bits - 16 bits, stable.  Keys become composites c = low_R(key) << 14 | i
-// (i = arrival index inside the bin), all distinct, so ordering composites is
-// the stable order.
-//  fast path: counting sort by the top `cb` of the R bits (cb = ceil(log2 m),
-//    <= 12; groups of ~1-2 keys) with shared atomics, then every key's final
-//    position = group start + #composites of its group below its own (groups
-//    <= 32 keys), written straight to the output;
-//  slow path (a group > 32 keys: low-entropy bins): stable LSD over the varying
-//    8-bit digits of the R bits on the permutation (warp multisplit ranks).
-// Output: keys[b0 + j] = (b << R) | (c_j >> 14), vals[b0 + j] = vals_in[b0 + i_j].
 // L2 bulk prefetch of the 16-byte-aligned part of [b, e) (never beyond it).
 FS_DEVINL void prefetch_l2_range(const void* b, const void* e) {
   const uintptr_t lo = ((uintptr_t)b + 15) & ~(uintptr_t)15, hi = (uintptr_t)e & ~(uintptr_t)15;
@@ -811,21 +871,29 @@ struct LocalSmemLayout {
 };
 static_assert(LocalSmemLayout::total <= 113 * 1024, "two CTAs per SM");
 
+// per-bin sort of Alg. 5 ("sort_bin"), stable: every key of
+// the bin lies in [top, top + 2^R) (a 16-bit bin: top = bin << R, R = key_bits -
+// 16; a recursion item: see wide_heavy.cuh) and is ordered by its offset
+// key - top.  Keys become composites c = (key - top) << 14 | i
+// (i = arrival index inside the bin), all distinct, so ordering composites is
+// the stable order.
+//  fast path: counting sort by the top `cb` of the R bits (cb = ceil(log2 m),
+//    <= 12; groups of ~1-2 keys) with shared atomics, then every key's final
+//    position = group start + #composites of its group below its own (groups
+//    <= 32 keys), written straight to the output;
+//  slow path (a group > 32 keys: low-entropy bins): stable LSD over the varying
+//    8-bit digits of the R bits on the permutation (warp multisplit ranks).
+// Output: kout[b0 + j] = top + (c_j >> 14), vout[b0 + j] = vin[b0 + i_j]; kin == kout
+// (in place) is allowed: every key is in registers before the first store.
 template <typename K, bool kHasValues>
-__global__ void __launch_bounds__(kLocalThreads, 2)
-    k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
-                 const MsdPlan* __restrict__ msd) {
-  if (!msd->use_msd) return;
-  const uint32_t bkt = blockIdx.x;
+__device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t b0,
+                                         uint32_t m, int R, K top) {
 #ifdef FS_SCATTER_STATS
   long long lph_t0 = clock64();
 #endif
-  const uint64_t b0 = __ldg(P16 + bkt);
-  const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
-  if (m <= 1) return;
   // The values are read only after the key phases: start pulling them into L2
   // now (4.38 vs 4.41 ms at c5; prefetching the bin one wave ahead did nothing).
-  if (kHasValues && threadIdx.x == 0) prefetch_l2_range(vals + b0, vals + b0 + m);
+  if (kHasValues && threadIdx.x == 0) prefetch_l2_range(vin + b0, vin + b0 + m);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* ck = reinterpret_cast<uint64_t*>(smem_raw + LocalSmemLayout::ck);
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::perm);
@@ -835,7 +903,6 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   __shared__ uint32_t wtot[kLocalWarps];
   __shared__ unsigned long long or_all, and_all;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint64_t low_mask = R >= 64 ? ~0ull : ((1ull << R) - 1);
 
   // counting digit: top cb of the R bits, cb = ceil(log2 m) capped
   int cb = 32 - __clz(m - 1);
@@ -854,7 +921,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const uint32_t i = tid + u * kLocalThreads;
-    cr[u] = i < m ? ((((uint64_t)keys[b0 + i]) & low_mask) << kIdxBits) | i : 0ull;
+    cr[u] = i < m ? (((uint64_t)(kin[b0 + i] - top)) << kIdxBits) | i : 0ull;
   }
   for (uint32_t w = tid; w < nwords; w += kLocalThreads) cntw[w] = 0;
   __syncthreads();
@@ -911,7 +978,6 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   // ---- final positions: group start + rank of the composite inside its group
   //      (cnt16[g] = end of group g); fin[position] = the composite's ck slot,
   //      so the keys are written out coalesced after the barrier.
-  const K top = (K)((uint64_t)bkt << R);
   uint16_t* fin = perm;
   // kRankU keys per thread at once: their group scans are independent shared
   // loads, interleaved (the loop runs to the longest of the kRankU groups).
@@ -1040,7 +1106,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 #pragma unroll 4
     for (uint32_t j = tid; j < m; j += kLocalThreads) {
       const uint64_t c = ck[pfinal[j]];
-      keys[b0 + j] = top | (K)(c >> kIdxBits);
+      kout[b0 + j] = top + (K)(c >> kIdxBits);
       pfinal[j] = (uint16_t)(c & ((1u << kIdxBits) - 1));
     }
   }
@@ -1053,7 +1119,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const uint32_t i = tid + u * kLocalThreads;
-      vr[u] = i < m ? vals[b0 + i] : 0u;
+      vr[u] = i < m ? vin[b0 + i] : 0u;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -1061,10 +1127,26 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
       if (i < m) sv[i] = vr[u];
     }
     __syncthreads();
-    for (uint32_t j = tid; j < m; j += kLocalThreads) vals[b0 + j] = sv[pfinal[j]];
+    for (uint32_t j = tid; j < m; j += kLocalThreads) vout[b0 + j] = sv[pfinal[j]];
   }
   FS_LPH(5);  // 5: values
 }
+
+// One CTA per 16-bit bin of the MSD path, in place in the output.  Bins above
+// the capacity are left to the recursion (k_heavy).
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kLocalThreads, 2)
+    k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
+                 const MsdPlan* __restrict__ msd) {
+  if (!msd->use_msd) return;
+  const uint32_t bkt = blockIdx.x;
+  const uint64_t b0 = __ldg(P16 + bkt);
+  const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
+  if (m <= 1 || m > (uint32_t)kLocalCap) return;
+  sort_bin<K, kHasValues>(keys, vals, keys, vals, b0, m, R, (K)((uint64_t)bkt << R));
+}
+
+#include "wide_heavy.cuh"
 
 // ================================================================ driver
 struct WideLayout {
@@ -1072,6 +1154,7 @@ struct WideLayout {
   size_t zero_begin = 0, spill = 0, l1spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0,
          zero_end = 0;
   size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
+  size_t hctl = 0, hseg0 = 0, hseg1 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // MSD recursion
   uint64_t tiles = 0, status_tiles = 0;
   uint64_t chunk_tiles = 0;  // MSD: tiles per histogram chunk (= level-1 virtual segment)
   int hgrid = 0;             // MSD: histogram CTAs = chunks
@@ -1108,6 +1191,8 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * (scan_tiles(kHistBins) + 1));
   L.tickets = off;
   off = align_up(off + sizeof(uint32_t) * kTickets);
+  L.hctl = off;
+  if (L.use_msd) off = align_up(off + sizeof(HeavyCtl));
   L.digit_hist = off;
   off = align_up(off + sizeof(unsigned long long) * kMaxPasses * kRadix);
   L.status = off;
@@ -1121,6 +1206,21 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   if (L.use_msd) off = align_up(off + sizeof(uint32_t) * kRadix * L.hgrid);
   L.vbase = off;
   if (L.use_msd) off = align_up(off + sizeof(uint64_t) * kRadix * L.hgrid);
+  if (L.use_msd) {
+    const HeavyCaps hc = heavy_caps(n);
+    L.hseg0 = off;
+    off = align_up(off + sizeof(HeavySeg) * hc.segs);
+    L.hseg1 = off;
+    off = align_up(off + sizeof(HeavySeg) * hc.segs);
+    L.hchunk = off;
+    off = align_up(off + sizeof(uint32_t) * hc.chunks);
+    L.hchist = off;
+    off = align_up(off + sizeof(uint32_t) * kRadix * hc.chunks);
+    L.hcbase = off;
+    off = align_up(off + sizeof(uint64_t) * kRadix * hc.chunks);
+    L.hitems = off;
+    off = align_up(off + sizeof(HeavyItem) * hc.items);
+  }
   L.lsd = off;
   off = align_up(off + sizeof(LsdPlan));
   L.msd = off;
@@ -1186,7 +1286,8 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     if ((e = launch_merge_scan(partials, L.hgrid, spill, nullptr, kHistBins, H16, kHistBins, 0, P16, scan_status,
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
-    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, (uint32_t)L.status_tiles, msd);
+    auto* hctl = (HeavyCtl*)(t + L.hctl);
+    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0));
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1208,6 +1309,40 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     k_local_sort<K, kHasValues><<<kHistBins, kLocalThreads, lsmem, s>>>(kout, vout, P16, key_bits - kTopBits, msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(4, s);
+    // ---- recursion into the bins above the local-sort capacity (returns at once if none)
+    HeavyArgs<K> ha{};
+    ha.kout = kout; ha.vout = vout; ha.kalt = alt_k; ha.valt = alt_v;
+    ha.kb = key_bits;
+    ha.levels = (key_bits - kTopBits + kRadixBits - 1) / kRadixBits;
+    ha.ctl = hctl;
+    ha.seg0 = (HeavySeg*)(t + L.hseg0);
+    ha.seg1 = (HeavySeg*)(t + L.hseg1);
+    ha.chunk_seg = (uint32_t*)(t + L.hchunk);
+    ha.chist = (uint32_t*)(t + L.hchist);
+    ha.cbase = (uint64_t*)(t + L.hcbase);
+    ha.items = (HeavyItem*)(t + L.hitems);
+    ha.msd = msd;
+    constexpr int hvsmem = (int)sizeof(HeavySmem<K, kHasValues>);
+    if ((e = cudaFuncSetAttribute(k_heavy<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize, hvsmem)) !=
+        cudaSuccess)
+      return e;
+    int hocc = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_heavy<K, kHasValues>, kHeavyThreads, hvsmem)) !=
+        cudaSuccess)
+      return e;
+    if (hocc < 1) return cudaErrorLaunchOutOfResources;
+    void* hargs[] = {&ha};
+    // Cooperative launch: every CTA co-resident, so the grid barriers are safe.
+    if ((e = cudaLaunchCooperativeKernel((const void*)k_heavy<K, kHasValues>, dim3((unsigned)(hocc * sms)),
+                                         dim3(kHeavyThreads), hargs, (size_t)hvsmem, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(k_heavy_items<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lsmem)) != cudaSuccess)
+      return e;
+    k_heavy_items<K, kHasValues><<<(unsigned)(2 * sms), kLocalThreads, lsmem, s>>>(
+        kout, vout, alt_k, alt_v, hctl, (const HeavyItem*)(t + L.hitems), msd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    phase_event(5, s);
   }
 
   // ---- LSD path (the fallback when MSD was planned; every kernel returns at once if MSD ran)
@@ -1216,7 +1351,7 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
   k_digit_hist<K><<<(unsigned)hgrid, 512, 0, s>>>(kin, n, passes, dhist, msd);
   k_digit_plan<<<1, kRadix, 0, s>>>(dhist, n, passes, lsd, msd);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int ev0 = L.use_msd ? 5 : 1;
+  const int ev0 = L.use_msd ? 6 : 1;
   phase_event(ev0, s);
   for (int p = 0; p < passes; ++p) {
     sa.mode = 0;

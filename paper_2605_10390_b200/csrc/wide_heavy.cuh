@@ -1,0 +1,334 @@
+// wide_heavy.cuh — recursion of the trie-binned MSD path into oversize bins
+// ("oversize bins recurse on the next digit").
+// Included once, by wide.cu, inside its anonymous namespace: it uses that
+// file's constants, match_digit8, digit_of and sort_bin.
+//
+// After the two MSD levels every key sits in its 16-bit bin, stably.  A bin
+// holding more than kLocalCap keys cannot be sorted in shared memory; it becomes
+// a "heavy segment" and is refined by further stable 8-bit MSD scatters on the
+// next digits (the bins of Alg. 5 are the leaves of the trie,
+// and a deeper trie level is the next digit), until every piece fits:
+//
+//   level r (digit bits [sh, sh + w), sh = kb - 16 - 8r, w = 8 or what is left)
+//     A. every heavy segment is split into nc <= kHeavyMaxChunks chunks;
+//     B. one CTA per chunk counts its keys' digits (chist[chunk][256]);
+//     C. one CTA per segment sums its chunks' counts (T[d]), scans them into the
+//        digit bases, gives every chunk its own per-digit start (cbase), and
+//        classifies the sub-bins [base_d, base_d + T[d]): heavy ones (> cap)
+//        become segments of level r+1; runs of the others are merged greedily
+//        into local-sort items of <= cap keys (sorted later by their low
+//        sh + 8 bits — or sh bits when the item is one sub-bin); a segment
+//        whose keys all share the digit is passed down without moving;
+//     D. CTAs take whole chunks and scatter them tile by tile in order, so the
+//        per-digit offsets are running sums in registers (no lookback).
+//   Phases are separated by grid-wide barriers of one cooperative kernel.
+// Then one kernel sorts every item (sort_bin) from where it lies into the
+// output.  Data ping-pong between the output and the temporary buffer per
+// segment (`buf`); items and the last level's segments that end in the
+// temporary buffer are written (sorted, or copied) into the output.
+//
+// Bounds (all buffers sized by the host from n): segments of a level are
+// disjoint and hold > cap keys each, so <= n / (cap + 1); chunks <= n /
+// kHeavyChunkKeys + segments; items of a level <= 2 n / cap + segments of this
+// and the next level + 1 (two consecutive greedy items hold > cap keys).
+#pragma once
+
+// (The records HeavySeg / HeavyItem / HeavyCtl and the capacities are defined in
+// wide.cu next to MsdPlan: k_msd_plan seeds the first level.)
+
+template <typename K, bool kHasValues>
+struct HeavySmem {
+  K keys[kHeavyTile];
+  uint32_t vals[kHasValues ? kHeavyTile : 1];
+  uint16_t whist[kHeavyWarps][kRadix];
+  unsigned long long gofs[kRadix];
+  uint32_t cnt[kRadix];
+  uint32_t wsum[kHeavyWarps];
+  uint32_t bcast;
+};
+
+// Segment records are rewritten by other CTAs between grid barriers: read them
+// through L2 (the L1 is not coherent).
+FS_DEVINL HeavySeg load_seg(const HeavySeg* p) {
+  HeavySeg g;
+  g.begin = __ldcg(&p->begin);
+  g.count = __ldcg(&p->count);
+  g.c0 = __ldcg(&p->c0);
+  g.nc = __ldcg(&p->nc);
+  g.buf = __ldcg(&p->buf);
+  g.skip = __ldcg(&p->skip);
+  return g;
+}
+
+// Copy items for [b, b + cnt) of the temporary buffer, in pieces.
+FS_DEVINL void emit_copy(HeavyCtl* ctl, HeavyItem* items, uint64_t b, uint64_t cnt) {
+  for (uint64_t o = 0; o < cnt; o += kHeavyCopyPiece)
+    items[atomicAdd(&ctl->nitems, 1u)] = HeavyItem{b + o, min(kHeavyCopyPiece, cnt - o), 0u, 0, 1};
+}
+
+// Block-wide exclusive scan over the 256 threads (one value each).
+FS_DEVINL uint64_t block_excl_scan256(uint64_t x, uint64_t* wsum64) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t inc = warp_inclusive_scan<uint64_t>(x);
+  if (lane == 31) wsum64[warp] = inc;
+  __syncthreads();
+  uint64_t off = 0;
+#pragma unroll
+  for (int w = 0; w < kHeavyWarps; ++w)
+    if (w < (int)warp) off += wsum64[w];
+  __syncthreads();
+  return off + inc - x;
+}
+
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<HeavySmem<K, kHasValues>*>(smem_raw);
+  __shared__ uint64_t wsum64[kHeavyWarps];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, d = tid;
+  const uint64_t gtid = blockIdx.x * (uint64_t)kHeavyThreads + tid, gthreads = (uint64_t)gridDim.x * kHeavyThreads;
+
+  if (!a.msd->use_msd) return;
+  for (int level = 0; level < a.levels; ++level) {
+    const int cur = level & 1;
+    const uint32_t S = __ldcg(&a.ctl->nseg[cur]);
+    if (S == 0) return;  // same value in every CTA (written before the last grid barrier)
+    HeavySeg* segs = cur ? a.seg1 : a.seg0;
+    HeavySeg* next = cur ? a.seg0 : a.seg1;
+    const int rem = a.kb - kTopBits - kRadixBits * level;  // bits below the digits done so far
+    const int w = rem < kRadixBits ? rem : kRadixBits;
+    const int sh = rem - w;
+    const uint32_t dmask = (1u << w) - 1u;
+
+    // ---- A. chunks of every segment
+    for (uint64_t s = gtid; s < S; s += gthreads) {
+      const uint64_t cnt = __ldcg(&segs[s].count);
+      uint64_t nc = (cnt + kHeavyChunkKeys - 1) / kHeavyChunkKeys;
+      nc = nc < 1 ? 1 : (nc > kHeavyMaxChunks ? kHeavyMaxChunks : nc);
+      const uint32_t c0 = atomicAdd(&a.ctl->nchunks[level], (uint32_t)nc);
+      segs[s].c0 = c0;
+      segs[s].nc = (uint32_t)nc;
+      for (uint32_t i = 0; i < (uint32_t)nc; ++i) a.chunk_seg[c0 + i] = (uint32_t)s;
+    }
+    grid.sync();
+    const uint32_t NC = __ldcg(&a.ctl->nchunks[level]);
+    auto chunk_range = [&](uint32_t c, const HeavySeg& sg, uint64_t& cb, uint64_t& ce) {
+      const uint64_t i = c - sg.c0;
+      cb = sg.begin + sg.count * i / sg.nc;
+      ce = sg.begin + sg.count * (i + 1) / sg.nc;
+    };
+
+    // ---- B. digit counts per chunk
+    for (uint32_t c = blockIdx.x; c < NC; c += gridDim.x) {
+      const HeavySeg sg = load_seg(segs + __ldcg(&a.chunk_seg[c]));
+      uint64_t cb, ce;
+      chunk_range(c, sg, cb, ce);
+      const K* src = sg.buf ? a.kalt : a.kout;
+      sm.cnt[d] = 0;
+      __syncthreads();
+      constexpr int kU = 8;  // loads in flight per thread
+      for (uint64_t j0 = cb + tid; j0 < ce; j0 += kU * kHeavyThreads) {
+        K kk[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) kk[u] = j0 + u * kHeavyThreads < ce ? __ldcg(src + j0 + u * kHeavyThreads) : K(0);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (j0 + u * kHeavyThreads < ce) atomicAdd(&sm.cnt[(uint32_t)(kk[u] >> sh) & dmask], 1u);
+      }
+      __syncthreads();
+      a.chist[(uint64_t)c * kRadix + d] = sm.cnt[d];
+      __syncthreads();
+    }
+    grid.sync();
+
+    // ---- C. bases, next-level segments, items
+    for (uint32_t s = blockIdx.x; s < S; s += gridDim.x) {
+      const HeavySeg sg = load_seg(segs + s);
+      uint64_t T = 0;
+#pragma unroll 8
+      for (uint32_t i = 0; i < sg.nc; ++i) T += __ldcg(&a.chist[(uint64_t)(sg.c0 + i) * kRadix + d]);
+      const int single = __syncthreads_or(T == sg.count);
+      const bool final_level = sh == 0;
+      if (single) {  // one digit: nothing moves at this level
+        if (tid == 0) {
+          segs[s].skip = 1;
+          if (!final_level) {
+            next[atomicAdd(&a.ctl->nseg[cur ^ 1], 1u)] = HeavySeg{sg.begin, sg.count, 0, 0, sg.buf, 0};
+          } else if (sg.buf) {  // sorted (the keys are equal): copy into the output
+            emit_copy(a.ctl, a.items, sg.begin, sg.count);
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      const uint64_t excl = block_excl_scan256(T, wsum64);
+      uint64_t run = sg.begin + excl;
+#pragma unroll 8
+      for (uint32_t i = 0; i < sg.nc; ++i) {
+        const uint64_t ci = (uint64_t)(sg.c0 + i) * kRadix + d;
+        a.cbase[ci] = run;
+        run += __ldcg(&a.chist[ci]);
+      }
+      sm.gofs[d] = T;  // digit counts for the classification below (thread 0)
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t dbuf = sg.buf ^ 1u;
+        if (final_level) {  // after this scatter the segment is sorted
+          if (dbuf) emit_copy(a.ctl, a.items, sg.begin, sg.count);
+        } else {
+          uint64_t pos = sg.begin, ib = 0;
+          uint32_t isz = 0, d0 = 0, d1 = 0;
+          // An item spanning digits d0..d1 holds keys in [top, top + (d1 - d0 + 1) << sh)
+          // with top = its first key's bits above sh: sorted by ceil(log2(span)) + sh bits,
+          // so a merged item's counting digit is not spent on the few digits it spans.
+          auto close = [&]() {
+            if (isz > 0) {
+              const uint32_t span = d1 - d0 + 1;
+              const uint32_t lg = span > 1 ? 32 - __clz(span - 1) : 0;
+              a.items[atomicAdd(&a.ctl->nitems, 1u)] =
+                  HeavyItem{ib, isz, (uint32_t)sh + lg, (uint16_t)sh, (uint16_t)dbuf};
+            }
+            isz = 0;
+          };
+          for (uint32_t dd = 0; dd <= dmask; ++dd) {
+            const uint64_t t = sm.gofs[dd];
+            if (t == 0) continue;
+            if (t > (uint64_t)kLocalCap) {
+              close();
+              next[atomicAdd(&a.ctl->nseg[cur ^ 1], 1u)] = HeavySeg{pos, t, 0, 0, dbuf, 0};
+            } else {
+              if (isz + t > (uint64_t)kLocalCap) close();
+              if (isz == 0) {
+                ib = pos;
+                d0 = dd;
+              }
+              isz += (uint32_t)t;
+              d1 = dd;
+            }
+            pos += t;
+          }
+          close();
+        }
+      }
+      __syncthreads();
+    }
+    grid.sync();
+
+    // ---- D. scatter: whole chunks per CTA, tiles in order, running offsets
+    for (;;) {
+      if (tid == 0) sm.bcast = atomicAdd(&a.ctl->ticket[level], 1u);
+      __syncthreads();
+      const uint32_t c = sm.bcast;
+      __syncthreads();
+      if (c >= NC) break;
+      const HeavySeg sg = load_seg(segs + __ldcg(&a.chunk_seg[c]));
+      if (sg.skip) continue;
+      uint64_t cb, ce;
+      chunk_range(c, sg, cb, ce);
+      const K* src_k = sg.buf ? a.kalt : a.kout;
+      const uint32_t* src_v = sg.buf ? a.valt : a.vout;
+      K* dst_k = sg.buf ? a.kout : a.kalt;
+      uint32_t* dst_v = sg.buf ? a.vout : a.valt;
+      uint64_t running = __ldcg(&a.cbase[(uint64_t)c * kRadix + d]);
+      for (int i = tid; i < kHeavyWarps * kRadix / 2; i += kHeavyThreads)
+        reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
+      __syncthreads();
+      for (uint64_t t0 = cb; t0 < ce; t0 += kHeavyTile) {
+        const uint32_t len = (uint32_t)min((uint64_t)kHeavyTile, ce - t0);
+        if (tid == 0 && t0 + kHeavyTile < ce) {  // warm L2 with the next tile while this one is ranked
+          const uint64_t ne = min(t0 + 2 * (uint64_t)kHeavyTile, ce);
+          prefetch_l2_range(src_k + t0 + kHeavyTile, src_k + ne);
+          if (kHasValues) prefetch_l2_range(src_v + t0 + kHeavyTile, src_v + ne);
+        }
+        K key[kHeavyItems];
+        uint32_t val[kHasValues ? kHeavyItems : 1];
+        const uint32_t e0 = warp * 32 * kHeavyItems + lane;
+#pragma unroll
+        for (int i = 0; i < kHeavyItems; ++i) {
+          const uint32_t e = e0 + 32 * i;
+          key[i] = e < len ? __ldcg(src_k + t0 + e) : K(0);
+          if (kHasValues) val[i] = e < len ? __ldcg(src_v + t0 + e) : 0u;
+        }
+        uint32_t rank[kHeavyItems];
+        uint16_t* wh = sm.whist[warp];
+#pragma unroll
+        for (int i = 0; i < kHeavyItems; ++i) {
+          const bool valid = e0 + 32 * i < len;
+          const uint32_t dg = (uint32_t)(key[i] >> sh) & dmask;
+          const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
+          const uint32_t leader = 31 - __clz(peers);
+          uint32_t old = 0;
+          if (valid && lane == leader) {
+            old = wh[dg];
+            wh[dg] = (uint16_t)(old + __popc(peers));
+          }
+          old = __shfl_sync(kFull, old, leader);
+          rank[i] = old + __popc(peers & lanemask_lt());
+          __syncwarp();
+        }
+        __syncthreads();
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int ww = 0; ww < kHeavyWarps; ++ww) {
+          const uint32_t x = sm.whist[ww][d];
+          sm.whist[ww][d] = (uint16_t)cnt;
+          cnt += x;
+        }
+        const uint32_t dstart = (uint32_t)block_excl_scan256(cnt, wsum64);
+#pragma unroll
+        for (int ww = 0; ww < kHeavyWarps; ++ww) sm.whist[ww][d] = (uint16_t)(sm.whist[ww][d] + dstart);
+        sm.gofs[d] = running - dstart;
+        running += cnt;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kHeavyItems; ++i) {
+          if (e0 + 32 * i < len) {
+            const uint32_t pos = wh[(uint32_t)(key[i] >> sh) & dmask] + rank[i];
+            sm.keys[pos] = key[i];
+            if (kHasValues) sm.vals[pos] = val[i];
+          }
+        }
+        __syncthreads();
+        for (uint32_t j = tid; j < len; j += kHeavyThreads) {
+          const K k = sm.keys[j];
+          const uint64_t dst = sm.gofs[(uint32_t)(k >> sh) & dmask] + j;
+          dst_k[dst] = k;
+          if (kHasValues) dst_v[dst] = sm.vals[j];
+        }
+        for (int i = tid; i < kHeavyWarps * kRadix / 2; i += kHeavyThreads)
+          reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    if (gtid == 0) a.ctl->nseg[cur] = 0;  // reused by level + 2 (written in its phase C, two barriers on)
+  }
+}
+
+// Every item: sorted (sort_bin) or copied from where it lies into the output.
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kLocalThreads, 2)
+    k_heavy_items(K* __restrict__ kout, uint32_t* __restrict__ vout, const K* __restrict__ kalt,
+                  const uint32_t* __restrict__ valt, const HeavyCtl* __restrict__ ctl,
+                  const HeavyItem* __restrict__ items, const MsdPlan* __restrict__ msd) {
+  if (!msd->use_msd) return;
+  const uint32_t ni = ctl->nitems;
+  for (uint32_t it = blockIdx.x; it < ni; it += gridDim.x) {
+    const HeavyItem item = items[it];
+    const K* sk = item.buf ? kalt : kout;
+    const uint32_t* sv = item.buf ? valt : vout;
+    if (item.R == 0 || item.count <= 1) {
+      if (item.buf)
+        for (uint64_t j = threadIdx.x; j < item.count; j += kLocalThreads) {
+          kout[item.begin + j] = sk[item.begin + j];
+          if (kHasValues) vout[item.begin + j] = sv[item.begin + j];
+        }
+    } else {
+      const K top = sk[item.begin] & (K)~((1ull << item.sh) - 1);
+      sort_bin<K, kHasValues>(sk, sv, kout, vout, item.begin, (uint32_t)item.count, (int)item.R, top);
+    }
+    __syncthreads();  // the shared memory of sort_bin is reused by the next item
+  }
+}

@@ -149,16 +149,85 @@ def test_msd_pairs_heavy_bins(cuda, distinct_low):
     np.testing.assert_array_equal(to_host(vo), ev)
 
 
-def test_msd_fallback_oversize_bin(cuda):
-    """One 16-bit bin above the local-sort capacity: the device takes the LSD path."""
+def _check_pairs(cuda, k, key_bits=64):
+    v = datagen.iota_u32(len(k))
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda), key_bits=key_bits)
+    ek, ev = oracle.sort_pairs_u64_u32(k, v, key_bits)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda), key_bits=key_bits)), ek)
+
+
+def test_msd_recursion_one_oversize_bin(cuda):
+    """One 16-bit bin above the local-sort capacity: it recurses on the next
+    digit while the other bins take the local sort."""
     n = (1 << 22) + 9
     k = datagen.gen_u64(n, seed=21)
     k[: 20_000] = (k[: 20_000] & np.uint64((1 << 48) - 1)) | np.uint64(0x1234 << 48)
-    v = datagen.iota_u32(n)
-    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
-    ek, ev = oracle.sort_pairs_u64_u32(k, v)
-    np.testing.assert_array_equal(to_host(ko), ek)
-    np.testing.assert_array_equal(to_host(vo), ev)
+    _check_pairs(cuda, k)
+
+
+@pytest.mark.parametrize("nhot", [1, 3, 64])
+def test_msd_recursion_many_oversize_bins(cuda, nhot):
+    """Half the keys in `nhot` hot 16-bit bins (one level of recursion splits
+    them), the rest spread over all bins."""
+    n = (1 << 22) + 13
+    k = datagen.gen_u64(n, seed=40 + nhot)
+    hot = datagen.gen_u64(n, seed=41) % np.uint64(2) == 0
+    tops = datagen.gen_u64(nhot, seed=42) >> np.uint64(48)
+    pick = tops[datagen.gen_u64(n, seed=43) % np.uint64(nhot)]
+    k[hot] = (k[hot] & np.uint64((1 << 48) - 1)) | (pick[hot] << np.uint64(48))
+    _check_pairs(cuda, k)
+
+
+def test_msd_recursion_deep(cuda):
+    """Hot bins whose next 16 bits are concentrated too: the recursion goes
+    several digits down before the pieces fit, with duplicate keys at the bottom."""
+    n = (1 << 22) + 3
+    k = datagen.gen_u64(n, seed=50)
+    sel = datagen.gen_u64(n, seed=51)
+    hot = sel % np.uint64(4) != 0
+    a = np.array([0x0001, 0xBEEF, 0x7F00], dtype=np.uint64)[sel % np.uint64(3)]
+    b = np.array([0x0000, 0x00FF, 0xFF00, 0x8001], dtype=np.uint64)[(sel >> np.uint64(8)) % np.uint64(4)]
+    low = (sel >> np.uint64(16)) % np.uint64(5000)  # many duplicates
+    k[hot] = (a[hot] << np.uint64(48)) | (b[hot] << np.uint64(32)) | low[hot]
+    _check_pairs(cuda, k)
+
+
+def test_msd_recursion_equal_keys(cuda):
+    """Oversize bins of equal keys: one that never moves (every digit uniform)
+    and one split once, whose halves then stay in the temporary buffer and are
+    copied out at the last level."""
+    n = (1 << 22) + 1
+    k = datagen.gen_u64(n, seed=60)
+    k[:30_000] = np.uint64(0xABCD_0123_4567_89AB)
+    k[30_000:60_000] = np.uint64(0x5555_1000_0000_0001)
+    k[60_000:90_000] = np.uint64(0x5555_2000_0000_0001)
+    k = k[datagen.gen_u64(n, seed=61).argsort(kind="stable")]
+    _check_pairs(cuda, k)
+
+
+@pytest.mark.parametrize("key_bits", [32, 37, 40, 48])
+def test_msd_recursion_key_bits(cuda, key_bits):
+    """Oversize bins at narrower key widths (the last digit shorter than 8 bits
+    when key_bits - 16 is not a multiple of 8); u32 keys too."""
+    n = (1 << 22) + 7
+    k = datagen.gen_u64(n, seed=70 + key_bits, key_bits=key_bits)
+    hot = datagen.gen_u64(n, seed=71) % np.uint64(3) == 0
+    k[hot] = (k[hot] & np.uint64((1 << (key_bits - 16)) - 1)) | np.uint64(0x00C3 << (key_bits - 16))
+    _check_pairs(cuda, k, key_bits)
+    if key_bits <= 32:
+        k32 = k.astype(np.uint32)
+        np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k32, cuda), key_bits=key_bits)),
+                                      oracle.sort_keys_u32(k32, key_bits))
+
+
+def test_msd_common_prefix_takes_lsd(cuda):
+    """Every key in one 16-bit bin (a common prefix): the device takes the LSD
+    path, which skips the uniform digits."""
+    n = (1 << 22) + 5
+    k = datagen.gen_u64(n, seed=80) & np.uint64((1 << 40) - 1)
+    _check_pairs(cuda, k)
 
 
 def test_msd_unaligned_buffers(cuda):
