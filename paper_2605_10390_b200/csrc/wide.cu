@@ -135,7 +135,8 @@ struct LsdPlan {
 struct MsdPlan {
   uint32_t use_msd;           // 1: MSD kernels run, LSD kernels return; 0: the reverse
   uint32_t l2_tiles;          // tiles of the level-2 pass
-  uint32_t l2_interleave;     // 1: level-2 tickets run across segments (t -> r = t / 256, s = t % 256)
+  uint32_t l2_interleave;     // 1: k_scatter runs level 2 with tickets across segments (t -> r = t / 256,
+                              //    s = t % 256); 0: too uneven, k_heavy runs it (level -1)
   uint32_t l2_rmax;           // most tiles in one segment
   uint32_t seg_tile0[kSegs + 1];
   uint64_t seg_begin[kSegs + 1];
@@ -167,9 +168,10 @@ struct HeavyItem {
 constexpr uint64_t kHeavyCopyPiece = 1ull << 20;  // copy items are emitted in pieces of this many keys
 
 struct HeavyCtl {
-  uint32_t nseg[2];                     // segments of the level with this parity
-  uint32_t nchunks[kHeavyMaxLevels];
-  uint32_t ticket[kHeavyMaxLevels];
+  uint32_t nseg[2];                         // segments of the level with this parity
+  uint32_t nl2;                             // segments of the uneven level-2 pass (level -1)
+  uint32_t nchunks[kHeavyMaxLevels + 1];    // per level + 1
+  uint32_t ticket[kHeavyMaxLevels + 1];
   uint32_t nitems;
 };
 
@@ -180,7 +182,7 @@ struct HeavyCaps {
 HeavyCaps heavy_caps(uint64_t n) {
   HeavyCaps c;
   c.segs = n / (kLocalCap + 1) + 1;
-  c.chunks = n / kHeavyChunkKeys + c.segs + 1;
+  c.chunks = n / kHeavyChunkKeys + c.segs + kSegs + 1;
   c.items = (uint64_t)kHeavyMaxLevels * (2 * (n / kLocalCap) + 2 * c.segs + 2 + n / kHeavyCopyPiece + c.segs);
   return c;
 }
@@ -191,9 +193,12 @@ struct HeavyArgs {
   uint32_t* vout;
   K* kalt;
   uint32_t* valt;
+  uint64_t n;
   int kb;      // key bits
   int levels;  // ceil((kb - 16) / 8)
+  int tma;     // every buffer 16-byte aligned: bulk-copy tiles
   HeavyCtl* ctl;
+  HeavySeg* segl2;  // level -1: the first-level buckets
   HeavySeg* seg0;  // segments of even levels
   HeavySeg* seg1;  // of odd levels
   uint32_t* chunk_seg;
@@ -404,7 +409,8 @@ __global__ void __launch_bounds__(256)
 // nothing) the LSD path runs instead, skipping its uniform digits.
 __global__ void __launch_bounds__(kSegs)
     k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
-               MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg) {
+               MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
+               HeavySeg* __restrict__ hl2) {
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
   __shared__ int one_bin;
@@ -441,13 +447,16 @@ __global__ void __launch_bounds__(kSegs)
     plan->l2_tiles = tot;
   }
   __syncthreads();
+  // Interleaved tickets keep every segment's lookback one tile deep; worth it
+  // unless the segments are so uneven that most tickets would be holes: then
+  // k_heavy runs level 2 over the buckets as segments (chunk histograms, no lookback).
+  const bool inter = (uint64_t)rmax * kSegs <= (uint64_t)status_cap;
   if (s == 0) {
     plan->use_msd = one_bin ? 0u : 1u;
     plan->l2_rmax = rmax;
-    // Interleaved tickets keep every segment's lookback one tile deep; worth it
-    // unless the segments are so uneven that most tickets would be holes.
-    plan->l2_interleave = (uint64_t)rmax * kSegs <= (uint64_t)status_cap ? 1u : 0u;
+    plan->l2_interleave = inter ? 1u : 0u;
   }
+  if (!inter && e > b) hl2[atomicAdd(&hctl->nl2, 1u)] = HeavySeg{b, e - b, 0, 0, 1, 0};
 }
 
 // ================================================================ scatter pass
@@ -477,7 +486,7 @@ struct ScatterArgs {
 };
 
 // Tile schedule.  Linear: ticket = tile index, the predecessor of a tile is the
-// previous tile (mode 0, and mode 2 with very uneven segments).  Interleaved
+// previous tile (mode 0).  Interleaved
 // (modes 1, 2): ticket t is tile r = t / nseg of segment s = t % nseg, so the
 // predecessor in the same segment was issued nseg tickets earlier and has
 // normally published its inclusive prefix: lookbacks stay one round deep
@@ -537,12 +546,13 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       inter = true;
       ntiles = a.l1_nseg * a.l1_chunk_tiles;
     } else {
+      if (!a.msd->l2_interleave) return;  // uneven buckets: k_heavy runs this level
       src_k = a.kB; src_v = a.vB; dst_k = a.kA; dst_v = a.vA;
       base_tab = a.P16;
       base_ss = 256;  // level 2: base[s][d] = P16[(s << 8) | d]
-      inter = a.msd->l2_interleave != 0;
-      nseg = inter ? kSegs : 1;
-      ntiles = inter ? kSegs * a.msd->l2_rmax : a.msd->l2_tiles;
+      inter = true;
+      nseg = kSegs;
+      ntiles = kSegs * a.msd->l2_rmax;
     }
   }
   const uint64_t n = a.n;
@@ -566,16 +576,6 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
         se = sm.seg_begin[t.seg + 1];
       }
       if (sb + (uint64_t)r * kSTile >= se) return false;
-    } else if (a.mode == 2) {
-      uint32_t lo = 0, hi = kSegs;  // largest s with seg_tile0[s] <= tile (a non-empty segment)
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (sm.seg_tile0[mid] <= tk) lo = mid; else hi = mid;
-      }
-      t.seg = lo;
-      r = tk - sm.seg_tile0[lo];
-      sb = sm.seg_begin[lo];
-      se = sm.seg_begin[lo + 1];
     } else {
       t.seg = 0;
       r = tk;
@@ -1154,7 +1154,7 @@ struct WideLayout {
   size_t zero_begin = 0, spill = 0, l1spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0,
          zero_end = 0;
   size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
-  size_t hctl = 0, hseg0 = 0, hseg1 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // MSD recursion
+  size_t hctl = 0, hseg0 = 0, hseg1 = 0, hsegl2 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // k_heavy
   uint64_t tiles = 0, status_tiles = 0;
   uint64_t chunk_tiles = 0;  // MSD: tiles per histogram chunk (= level-1 virtual segment)
   int hgrid = 0;             // MSD: histogram CTAs = chunks
@@ -1212,6 +1212,8 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
     off = align_up(off + sizeof(HeavySeg) * hc.segs);
     L.hseg1 = off;
     off = align_up(off + sizeof(HeavySeg) * hc.segs);
+    L.hsegl2 = off;
+    off = align_up(off + sizeof(HeavySeg) * kSegs);
     L.hchunk = off;
     off = align_up(off + sizeof(uint32_t) * hc.chunks);
     L.hchist = off;
@@ -1287,7 +1289,8 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
     auto* hctl = (HeavyCtl*)(t + L.hctl);
-    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0));
+    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0),
+                                   (HeavySeg*)(t + L.hsegl2));
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1302,19 +1305,16 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       phase_event(1 + level, s);
     }
-    constexpr int lsmem = LocalSmemLayout::total;
-    if ((e = cudaFuncSetAttribute(k_local_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lsmem)) != cudaSuccess)
-      return e;
-    k_local_sort<K, kHasValues><<<kHistBins, kLocalThreads, lsmem, s>>>(kout, vout, P16, key_bits - kTopBits, msd);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    phase_event(4, s);
-    // ---- recursion into the bins above the local-sort capacity (returns at once if none)
+    // ---- k_heavy: level 2 of uneven buckets, then the recursion into the bins
+    //      above the local-sort capacity (returns at once if there is neither)
     HeavyArgs<K> ha{};
     ha.kout = kout; ha.vout = vout; ha.kalt = alt_k; ha.valt = alt_v;
+    ha.n = n;
     ha.kb = key_bits;
     ha.levels = (key_bits - kTopBits + kRadixBits - 1) / kRadixBits;
+    ha.tma = tma ? 1 : 0;
     ha.ctl = hctl;
+    ha.segl2 = (HeavySeg*)(t + L.hsegl2);
     ha.seg0 = (HeavySeg*)(t + L.hseg0);
     ha.seg1 = (HeavySeg*)(t + L.hseg1);
     ha.chunk_seg = (uint32_t*)(t + L.hchunk);
@@ -1336,6 +1336,14 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     if ((e = cudaLaunchCooperativeKernel((const void*)k_heavy<K, kHasValues>, dim3((unsigned)(hocc * sms)),
                                          dim3(kHeavyThreads), hargs, (size_t)hvsmem, s)) != cudaSuccess)
       return e;
+    phase_event(4, s);
+    // ---- per-bin sorts: the 16-bit bins that fit, then the recursion's items
+    constexpr int lsmem = LocalSmemLayout::total;
+    if ((e = cudaFuncSetAttribute(k_local_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lsmem)) != cudaSuccess)
+      return e;
+    k_local_sort<K, kHasValues><<<kHistBins, kLocalThreads, lsmem, s>>>(kout, vout, P16, key_bits - kTopBits, msd);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_heavy_items<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lsmem)) != cudaSuccess)
       return e;

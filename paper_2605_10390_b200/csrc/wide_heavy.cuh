@@ -1,7 +1,8 @@
 // wide_heavy.cuh — recursion of the trie-binned MSD path into oversize bins
-// ("oversize bins recurse on the next digit").
+// ("oversize bins recurse on the next digit"), and the
+// level-2 scatter of very uneven first-level buckets.
 // Included once, by wide.cu, inside its anonymous namespace: it uses that
-// file's constants, match_digit8, digit_of and sort_bin.
+// file's constants, match_digit8, the bulk-copy helpers and sort_bin.
 //
 // After the two MSD levels every key sits in its 16-bit bin, stably.  A bin
 // holding more than kLocalCap keys cannot be sorted in shared memory; it becomes
@@ -9,19 +10,24 @@
 // next digits (the bins of Alg. 5 are the leaves of the trie,
 // and a deeper trie level is the next digit), until every piece fits:
 //
-//   level r (digit bits [sh, sh + w), sh = kb - 16 - 8r, w = 8 or what is left)
-//     A. every heavy segment is split into nc <= kHeavyMaxChunks chunks;
+//   level r >= 0 (digit bits [sh, sh + w), sh = kb - 24 - 8r, w = 8 or what is left)
+//     A. every segment is split into nc <= kHeavyMaxChunks chunks;
 //     B. one CTA per chunk counts its keys' digits (chist[chunk][256]);
 //     C. one CTA per segment sums its chunks' counts (T[d]), scans them into the
 //        digit bases, gives every chunk its own per-digit start (cbase), and
 //        classifies the sub-bins [base_d, base_d + T[d]): heavy ones (> cap)
 //        become segments of level r+1; runs of the others are merged greedily
-//        into local-sort items of <= cap keys (sorted later by their low
-//        sh + 8 bits — or sh bits when the item is one sub-bin); a segment
-//        whose keys all share the digit is passed down without moving;
+//        into local-sort items of <= cap keys; a segment whose keys all share
+//        the digit is passed down without moving;
 //     D. CTAs take whole chunks and scatter them tile by tile in order, so the
-//        per-digit offsets are running sums in registers (no lookback).
+//        per-digit offsets are running sums in registers (no lookback); the
+//        next tile is bulk-copied (TMA) into the second shared buffer while
+//        the current one is ranked, reordered and written.
 //   Phases are separated by grid-wide barriers of one cooperative kernel.
+//   Level -1 (only when k_msd_plan found the first-level buckets too uneven for
+//   the interleaved lookback of k_scatter mode 2): the same A-D over the 256
+//   buckets with the second digit, from the temporary buffer into the output,
+//   without classification (the 16-bit bins are already planned).
 // Then one kernel sorts every item (sort_bin) from where it lies into the
 // output.  Data ping-pong between the output and the temporary buffer per
 // segment (`buf`); items and the last level's segments that end in the
@@ -30,7 +36,8 @@
 // Bounds (all buffers sized by the host from n): segments of a level are
 // disjoint and hold > cap keys each, so <= n / (cap + 1); chunks <= n /
 // kHeavyChunkKeys + segments; items of a level <= 2 n / cap + segments of this
-// and the next level + 1 (two consecutive greedy items hold > cap keys).
+// and the next level + 1 (two consecutive greedy items hold > cap keys), plus
+// the copy pieces.
 #pragma once
 
 // (The records HeavySeg / HeavyItem / HeavyCtl and the capacities are defined in
@@ -38,12 +45,12 @@
 
 template <typename K, bool kHasValues>
 struct HeavySmem {
-  K keys[kHeavyTile];
-  uint32_t vals[kHasValues ? kHeavyTile : 1];
+  K keys[2][kHeavyTile + kSlack];
+  uint32_t vals[2][kHasValues ? kHeavyTile + kSlack : 1];
   uint16_t whist[kHeavyWarps][kRadix];
   unsigned long long gofs[kRadix];
   uint32_t cnt[kRadix];
-  uint32_t wsum[kHeavyWarps];
+  uint64_t mbar[2];
   uint32_t bcast;
 };
 
@@ -89,14 +96,29 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
   __shared__ uint64_t wsum64[kHeavyWarps];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, d = tid;
   const uint64_t gtid = blockIdx.x * (uint64_t)kHeavyThreads + tid, gthreads = (uint64_t)gridDim.x * kHeavyThreads;
-
   if (!a.msd->use_msd) return;
-  for (int level = 0; level < a.levels; ++level) {
+  const uint64_t n_al = a.n & ~(uint64_t)3;  // bulk copies never read past this
+  if (tid == 0) {
+    mbar_init(&sm.mbar[0], 1);
+    mbar_init(&sm.mbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t par = 0;           // bit b: parity of the next phase of buffer b's mbarrier (uniform over the CTA)
+  uint32_t nb = 0;            // buffer of the next tile
+
+  for (int level = -1; level < a.levels; ++level) {
+    const bool l2 = level < 0;  // the uneven level-2 pass
     const int cur = level & 1;
-    const uint32_t S = __ldcg(&a.ctl->nseg[cur]);
-    if (S == 0) return;  // same value in every CTA (written before the last grid barrier)
-    HeavySeg* segs = cur ? a.seg1 : a.seg0;
+    HeavySeg* segs = l2 ? a.segl2 : (cur ? a.seg1 : a.seg0);
     HeavySeg* next = cur ? a.seg0 : a.seg1;
+    uint32_t* nseg_p = l2 ? &a.ctl->nl2 : &a.ctl->nseg[cur];
+    const uint32_t S = __ldcg(nseg_p);
+    if (S == 0) {
+      if (l2) continue;
+      return;  // same value in every CTA (written before the last grid barrier)
+    }
+    const int slot = level + 1;
     const int rem = a.kb - kTopBits - kRadixBits * level;  // bits below the digits done so far
     const int w = rem < kRadixBits ? rem : kRadixBits;
     const int sh = rem - w;
@@ -107,13 +129,13 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
       const uint64_t cnt = __ldcg(&segs[s].count);
       uint64_t nc = (cnt + kHeavyChunkKeys - 1) / kHeavyChunkKeys;
       nc = nc < 1 ? 1 : (nc > kHeavyMaxChunks ? kHeavyMaxChunks : nc);
-      const uint32_t c0 = atomicAdd(&a.ctl->nchunks[level], (uint32_t)nc);
+      const uint32_t c0 = atomicAdd(&a.ctl->nchunks[slot], (uint32_t)nc);
       segs[s].c0 = c0;
       segs[s].nc = (uint32_t)nc;
       for (uint32_t i = 0; i < (uint32_t)nc; ++i) a.chunk_seg[c0 + i] = (uint32_t)s;
     }
     grid.sync();
-    const uint32_t NC = __ldcg(&a.ctl->nchunks[level]);
+    const uint32_t NC = __ldcg(&a.ctl->nchunks[slot]);
     auto chunk_range = [&](uint32_t c, const HeavySeg& sg, uint64_t& cb, uint64_t& ce) {
       const uint64_t i = c - sg.c0;
       cb = sg.begin + sg.count * i / sg.nc;
@@ -133,6 +155,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
         K kk[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) kk[u] = j0 + u * kHeavyThreads < ce ? __ldcg(src + j0 + u * kHeavyThreads) : K(0);
+        // (Warp-aggregating equal digits measured slower, even on one-digit segments.)
 #pragma unroll
         for (int u = 0; u < kU; ++u)
           if (j0 + u * kHeavyThreads < ce) atomicAdd(&sm.cnt[(uint32_t)(kk[u] >> sh) & dmask], 1u);
@@ -144,13 +167,13 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
     grid.sync();
 
     // ---- C. bases, next-level segments, items
+    const bool final_level = sh == 0;
     for (uint32_t s = blockIdx.x; s < S; s += gridDim.x) {
       const HeavySeg sg = load_seg(segs + s);
       uint64_t T = 0;
 #pragma unroll 8
       for (uint32_t i = 0; i < sg.nc; ++i) T += __ldcg(&a.chist[(uint64_t)(sg.c0 + i) * kRadix + d]);
-      const int single = __syncthreads_or(T == sg.count);
-      const bool final_level = sh == 0;
+      const int single = l2 ? 0 : __syncthreads_or(T == sg.count);
       if (single) {  // one digit: nothing moves at this level
         if (tid == 0) {
           segs[s].skip = 1;
@@ -171,7 +194,8 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
         a.cbase[ci] = run;
         run += __ldcg(&a.chist[ci]);
       }
-      sm.gofs[d] = T;  // digit counts for the classification below (thread 0)
+      if (l2) continue;  // the 16-bit bins were planned by k_msd_plan
+      sm.gofs[d] = T;    // digit counts for the classification below (thread 0)
       __syncthreads();
       if (tid == 0) {
         const uint32_t dbuf = sg.buf ^ 1u;
@@ -218,7 +242,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
 
     // ---- D. scatter: whole chunks per CTA, tiles in order, running offsets
     for (;;) {
-      if (tid == 0) sm.bcast = atomicAdd(&a.ctl->ticket[level], 1u);
+      if (tid == 0) sm.bcast = atomicAdd(&a.ctl->ticket[slot], 1u);
       __syncthreads();
       const uint32_t c = sm.bcast;
       __syncthreads();
@@ -234,22 +258,58 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
       uint64_t running = __ldcg(&a.cbase[(uint64_t)c * kRadix + d]);
       for (int i = tid; i < kHeavyWarps * kRadix / 2; i += kHeavyThreads)
         reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
+      // The tile starting at t0 -> buffer b: a bulk copy of the 16-byte-aligned
+      // span covering it (thread 0), completing on mbar[b].
+      auto issue = [&](uint64_t t0, int b) {
+        const uint64_t t1 = min(t0 + (uint64_t)kHeavyTile, ce);
+        const uint64_t abeg = t0 & ~(uint64_t)3, aend = min((t1 + 3) & ~(uint64_t)3, n_al);
+        const uint32_t cnt = aend > abeg ? (uint32_t)(aend - abeg) : 0u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&sm.mbar[b], cnt * (uint32_t)(sizeof(K) + (kHasValues ? 4 : 0)));
+        if (cnt) {
+          bulk_g2s(sm.keys[b], src_k + abeg, cnt * (uint32_t)sizeof(K), &sm.mbar[b]);
+          if (kHasValues) bulk_g2s(sm.vals[b], src_v + abeg, cnt * 4u, &sm.mbar[b]);
+        }
+      };
+      if (a.tma && tid == 0) issue(cb, (int)nb);
       __syncthreads();
       for (uint64_t t0 = cb; t0 < ce; t0 += kHeavyTile) {
+        const int b = (int)nb;
+        nb ^= 1u;
         const uint32_t len = (uint32_t)min((uint64_t)kHeavyTile, ce - t0);
-        if (tid == 0 && t0 + kHeavyTile < ce) {  // warm L2 with the next tile while this one is ranked
-          const uint64_t ne = min(t0 + 2 * (uint64_t)kHeavyTile, ce);
-          prefetch_l2_range(src_k + t0 + kHeavyTile, src_k + ne);
-          if (kHasValues) prefetch_l2_range(src_v + t0 + kHeavyTile, src_v + ne);
+        K* kbuf = sm.keys[b];
+        uint32_t* vbuf = kHasValues ? sm.vals[b] : nullptr;
+        uint32_t off = 0;
+        if (a.tma) {
+          if (tid == 0 && t0 + kHeavyTile < ce) issue(t0 + kHeavyTile, b ^ 1);
+          mbar_wait(&sm.mbar[b], (par >> b) & 1u);
+          off = (uint32_t)(t0 & 3);
+          // keys past the last 16-byte boundary of the array (< 4): plain loads
+          const uint64_t t1 = t0 + len, covered = max(min((t1 + 3) & ~(uint64_t)3, n_al), t0);
+          if (covered < t1) {
+            const uint32_t e0 = (uint32_t)(covered - t0);
+            if (tid < len - e0) {
+              kbuf[off + e0 + tid] = src_k[covered + tid];
+              if (kHasValues) vbuf[off + e0 + tid] = src_v[covered + tid];
+            }
+            __syncthreads();
+          }
+        } else {
+          for (uint32_t e = tid; e < len; e += kHeavyThreads) {
+            kbuf[e] = __ldcg(src_k + t0 + e);
+            if (kHasValues) vbuf[e] = __ldcg(src_v + t0 + e);
+          }
+          __syncthreads();
         }
+        par ^= 1u << b;
         K key[kHeavyItems];
         uint32_t val[kHasValues ? kHeavyItems : 1];
         const uint32_t e0 = warp * 32 * kHeavyItems + lane;
 #pragma unroll
         for (int i = 0; i < kHeavyItems; ++i) {
           const uint32_t e = e0 + 32 * i;
-          key[i] = e < len ? __ldcg(src_k + t0 + e) : K(0);
-          if (kHasValues) val[i] = e < len ? __ldcg(src_v + t0 + e) : 0u;
+          key[i] = e < len ? kbuf[off + e] : K(0);
+          if (kHasValues) val[i] = e < len ? vbuf[off + e] : 0u;
         }
         uint32_t rank[kHeavyItems];
         uint16_t* wh = sm.whist[warp];
@@ -282,28 +342,29 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
         sm.gofs[d] = running - dstart;
         running += cnt;
         __syncthreads();
+        // reorder through shared memory (the tile's buffer becomes the stage)
 #pragma unroll
         for (int i = 0; i < kHeavyItems; ++i) {
           if (e0 + 32 * i < len) {
             const uint32_t pos = wh[(uint32_t)(key[i] >> sh) & dmask] + rank[i];
-            sm.keys[pos] = key[i];
-            if (kHasValues) sm.vals[pos] = val[i];
+            kbuf[pos] = key[i];
+            if (kHasValues) vbuf[pos] = val[i];
           }
         }
         __syncthreads();
         for (uint32_t j = tid; j < len; j += kHeavyThreads) {
-          const K k = sm.keys[j];
+          const K k = kbuf[j];
           const uint64_t dst = sm.gofs[(uint32_t)(k >> sh) & dmask] + j;
           dst_k[dst] = k;
-          if (kHasValues) dst_v[dst] = sm.vals[j];
+          if (kHasValues) dst_v[dst] = vbuf[j];
         }
         for (int i = tid; i < kHeavyWarps * kRadix / 2; i += kHeavyThreads)
           reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0;
-        __syncthreads();
+        __syncthreads();  // the buffer is free for the copy after next
       }
     }
     grid.sync();
-    if (gtid == 0) a.ctl->nseg[cur] = 0;  // reused by level + 2 (written in its phase C, two barriers on)
+    if (gtid == 0 && !l2) a.ctl->nseg[cur] = 0;  // reused by level + 2 (written in its phase C, two barriers on)
   }
 }
 

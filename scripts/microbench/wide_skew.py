@@ -80,7 +80,7 @@ for path in libs:
         print(f"{os.path.basename(path):24s} {kind:10s} {statistics.median(ts):8.3f} ms  "
               f"{n / statistics.median(ts) / 1e6:7.2f} Gpairs/s  ordered={ordered} perm={perm} stable={stable}  "
               + " ".join(f"{nm}={evs[i].elapsed_time(evs[i + 1]):.2f}" for i, nm in
-                         enumerate(["hist", "L1", "L2", "local", "heavy"])) + f" lsd={evs[5].elapsed_time(evs[15]):.2f}",
+                         enumerate(["hist", "L1", "L2", "k_heavy", "local"])) + f" lsd={evs[5].elapsed_time(evs[15]):.2f}",
               flush=True)
         del k, v, ko, vo
     del temp

@@ -288,8 +288,9 @@ def test_fuzz_pairs_and_keys(cuda, case):
 
 def test_msd_level2_linear_order(cuda):
     """A first-level bucket holding 30% of the keys (bins still fit the local
-    sort): 256 x (its tiles) exceeds the status rows, so level 2 runs its tiles in
-    linear order with segment-start lookbacks instead of interleaved tickets."""
+    sort): 256 x (its tiles) exceeds the status rows, so level 2 is not run by
+    the interleaved k_scatter but by k_heavy over the buckets as segments
+    (per-chunk digit histograms, CTA-owned chunks, no lookback)."""
     n = (1 << 22) + 5
     k = datagen.gen_u64(n, seed=77)
     hot = datagen.gen_u64(n, seed=78) % np.uint64(10) < np.uint64(3)
