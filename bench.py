@@ -214,8 +214,9 @@ def run_fs_pairs(args, dev):
     temp = torch.empty(L.fs_sort_pairs_u64_u32_temp_bytes(n, 64), dtype=torch.uint8, device=dev)
     # phase events (include/fractalsort.h): MSD-planned sorts record [0] start,
     # [1] trie histogram + scan + plan, [2] level-1 scatter, [3] level-2 scatter,
-    # [4] per-bin local sort, [5] recursion into oversize bins, [6..15] the LSD
-    # kernels (they return at once when the MSD path ran).
+    # [4] k_heavy (uneven level 2 and the recursion into oversize bins; returns
+    # at once on c5), [5] per-bin local sorts, [6..15] the LSD kernels (they
+    # return at once when the MSD path ran).
     nev = 16
     steps = args.steps
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(steps)]
@@ -241,12 +242,12 @@ def run_fs_pairs(args, dev):
         torch.cuda.synchronize()
     total_ms = events[0][0].elapsed_time(events[-1][nev - 1])
     phase = [statistics.mean(r[i].elapsed_time(r[i + 1]) for r in events) for i in range(nev - 1)]
-    names = ["trie_hist+scan+plan", "msd_level1_scatter", "msd_level2_scatter", "local_sort", "msd_recursion",
+    names = ["trie_hist+scan+plan", "msd_level1_scatter", "msd_level2_scatter", "k_heavy", "local_sort",
              "lsd_digit_hist+plan"] + [f"lsd_pass{i}" for i in range(8)] + ["lsd_identity_copy"]
     lsd_ms = sum(phase[5:])
-    path = "msd" if phase[3] > lsd_ms else "lsd-fallback"
+    path = "msd" if phase[4] > lsd_ms else "lsd"
     # dominant kernel: each MSD pass reads and writes 8 B key + 4 B value per pair
-    cand = [1, 2, 3] if path == "msd" else list(range(6, 14))
+    cand = [1, 2, 4] if path == "msd" else list(range(6, 14))
     dom = max(cand, key=lambda i: phase[i])
     peak, peak_src = measured_peak_gbs()
     alg = 24 * n

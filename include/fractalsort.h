@@ -107,8 +107,10 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
  *    leaf level of a 16-level compressed trie over the top 16 key bits; its
  *    level-8 and level-16 counters bound two stable 8-bit MSD scatters; every
  *    16-bit bin is then sorted by its remaining bits in shared memory (Alg. 5's
- *    bins and per-bin sort).  Taken when every bin
- *    holds <= 8,704 keys — decided on the device, no host synchronisation;
+ *    bins and per-bin sort).  A bin above 8,704 keys
+ *    recurses on the next 8-bit digits (stable MSD scatters of its own) until
+ *    every piece fits.  Taken unless one 16-bit bin holds every key (a common
+ *    prefix) — decided on the device, no host synchronisation;
  *  - otherwise stable LSD radix ("histogram, prefix sum and stable scatter
  *    phases", §II) with 8-bit digits and one compressed histogram
  *    per digit, all digit histograms in one read pass (config c5's "multi-digit
@@ -296,9 +298,10 @@ fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out,
  *                      kernel;
  *   wide sorts, MSD planned (n >= 2^22, key_bits >= 32): [0] start, [1] after
  *                      the trie histogram + scan + plan, [2] level-1 scatter,
- *                      [3] level-2 scatter, [4] per-bin sort, [5] recursion
- *                      into the bins above the local-sort capacity (returns at
- *                      once if there are none), [6] after the LSD digit
+ *                      [3] level-2 scatter, [4] k_heavy: level 2 of uneven
+ *                      first-level buckets and the recursion into the bins
+ *                      above the local-sort capacity (returns at once if there
+ *                      is neither), [5] per-bin sorts, [6] after the LSD digit
  *                      histograms (they return at once when MSD ran), [7 + p]
  *                      after LSD pass p, last after the identity copy;
  *   wide sorts, LSD only: [0] start, [1] after the digit histograms + plan,

@@ -20,14 +20,21 @@
 //          within each of the 256 first-level segments, into the output.
 //       c. k_local_sort: every 16-bit bin (<= kLocalCap keys) is sorted in
 //          shared memory by its remaining kb-16 bits, stably, in place.
-//     Traffic: 8 (u64 key read) + 3 x 24 = 80 B/pair for c5 (vs 200 for LSD-8).
-// (2) Stable LSD with 8-bit digits (fallback, and small n / narrow keys): one
-//     read builds all digit histograms (k_digit_hist), k_digit_plan scans them
-//     and skips single-bin digits, then one k_scatter (mode 0) per digit.
+//       d. k_heavy (wide_heavy.cuh): bins above kLocalCap recurse on the next
+//          8-bit digits until every piece fits; k_heavy_items sorts the pieces.
+//          k_heavy also runs level 2 when the first-level buckets are too
+//          uneven for the interleaved lookback of (b).
+//     Traffic: 8 (u64 key read) + 3 x 24 = 80 B/pair for c5 (vs 200 for LSD-8);
+//     each recursion level adds 8 + 24 B per pair of the oversize bins.
+// (2) Stable LSD with 8-bit digits (small n / narrow keys, and a common 16-bit
+//     prefix): one read builds all digit histograms (k_digit_hist),
+//     k_digit_plan scans them and skips single-bin digits, then one k_scatter
+//     (mode 0) per digit.
 //
-// Choice: the MSD path is taken iff every 16-bit bin holds <= kLocalCap keys —
-// decided on the device (k_msd_plan), so nothing synchronises with the host;
-// the kernels of the path not taken return at once.
+// Choice: the MSD path is taken unless one 16-bit bin holds every key (then the
+// MSD levels would move everything for nothing and LSD skips the uniform
+// digits) — decided on the device (k_msd_plan), so nothing synchronises with
+// the host; the kernels of the path not taken return at once.
 //
 // k_scatter (the "histogram, prefix sum and stable scatter phases"):
 // persistent CTAs (2 per SM for pairs) take 4,096-key tiles in order from an
@@ -1353,7 +1360,7 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     phase_event(5, s);
   }
 
-  // ---- LSD path (the fallback when MSD was planned; every kernel returns at once if MSD ran)
+  // ---- LSD path (when MSD was planned: taken only for a common 16-bit prefix; else every kernel returns at once)
   uint64_t hgrid = (n + 511) / 512;
   if (hgrid > (uint64_t)sms * 4) hgrid = (uint64_t)sms * 4;
   k_digit_hist<K><<<(unsigned)hgrid, 512, 0, s>>>(kin, n, passes, dhist, msd);

@@ -12,6 +12,8 @@ for w in c1 c3a c3b c3c c3d; do timeout 600 python bench.py --workload $w --step
 timeout 900 python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err; tail -c 300 $O/bench_c5.json
 timeout 900 python bench.py --workload c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c4_1gpu.json 2> $O/bench_c4.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+rm -f scripts/microbench/variants/*.so
+timeout 600 python scripts/microbench/wide_skew.py $((1 << 29)) > $O/wide_skew_c5size.txt 2>&1
 NB="--no-e2e --no-cpu-baseline --no-verify"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 5 --warmup 3 $NB > $O/ncu_launch_c2.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c5.csv python bench.py --workload c5 --steps 2 --warmup 1 $NB > $O/ncu_launch_c5.log 2>&1
