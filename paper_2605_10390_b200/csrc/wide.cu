@@ -457,7 +457,11 @@ __global__ void __launch_bounds__(kSegs)
   // Interleaved tickets keep every segment's lookback one tile deep; worth it
   // unless the segments are so uneven that most tickets would be holes: then
   // k_heavy runs level 2 over the buckets as segments (chunk histograms, no lookback).
+#ifdef FS_FORCE_L2_HEAVY  // timing experiment: level 2 always in k_heavy
+  const bool inter = false && status_cap;
+#else
   const bool inter = (uint64_t)rmax * kSegs <= (uint64_t)status_cap;
+#endif
   if (s == 0) {
     plan->use_msd = one_bin ? 0u : 1u;
     plan->l2_rmax = rmax;
