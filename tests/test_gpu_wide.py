@@ -222,6 +222,37 @@ def test_msd_recursion_key_bits(cuda, key_bits):
                                       oracle.sort_keys_u32(k32, key_bits))
 
 
+def test_msd_recursion_unaligned_buffers(cuda):
+    """Oversize bins and uneven first-level buckets with buffers that are not
+    16-byte aligned: k_heavy loads its tiles without bulk copies."""
+    n = (1 << 22) + 11
+    k = datagen.gen_u64(n + 1, seed=90)
+    hot = datagen.gen_u64(n + 1, seed=91) % np.uint64(5) < np.uint64(2)
+    k[hot] = (k[hot] & np.uint64((1 << 48) - 1)) | np.uint64(0x9ABC << 48)
+    v = datagen.iota_u32(n + 1)
+    kd, vd = to_dev(k, cuda)[1:], to_dev(v, cuda)[1:]
+    ko, vo = fs.sort_pairs(kd, vd)
+    ek, ev = oracle.sort_pairs_u64_u32(k[1:], v[1:])
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
+def test_msd_recursion_many_small_oversize_bins(cuda):
+    """Hundreds of bins just above the capacity (8,705 to 9,000 keys): one chunk
+    per segment, sub-bins merged into items."""
+    n = (1 << 22) + 2
+    k = datagen.gen_u64(n, seed=95)
+    nb = 400
+    sizes = 8705 + (datagen.gen_u64(nb, seed=96) % np.uint64(296)).astype(np.int64)
+    tops = (np.arange(nb, dtype=np.uint64) * np.uint64(163)) << np.uint64(48)
+    pos = 0
+    for t, m in zip(tops, sizes):
+        k[pos:pos + m] = (k[pos:pos + m] & np.uint64((1 << 48) - 1)) | t
+        pos += int(m)
+    k = k[datagen.gen_u64(n, seed=97).argsort(kind="stable")]
+    _check_pairs(cuda, k)
+
+
 def test_msd_common_prefix_takes_lsd(cuda):
     """Every key in one 16-bit bin (a common prefix): the device takes the LSD
     path, which skips the uniform digits."""
