@@ -109,8 +109,11 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
  *    16-bit bin is then sorted by its remaining bits in shared memory (Alg. 5's
  *    bins and per-bin sort).  A bin above 8,704 keys
  *    recurses on the next 8-bit digits (stable MSD scatters of its own) until
- *    every piece fits.  Taken unless one 16-bit bin holds every key (a common
- *    prefix) — decided on the device, no host synchronisation;
+ *    every piece fits.  If the keys share a prefix (the bits where some keys
+ *    differ end at hb < key_bits - 1) and hb + 1 >= 32, the 16 bins' window is
+ *    moved to [hb - 15, hb] (the trie histogram is rebuilt there).  With fewer
+ *    than 32 varying bits the LSD scheme below is taken — all decided on the
+ *    device, no host synchronisation;
  *  - otherwise stable LSD radix ("histogram, prefix sum and stable scatter
  *    phases", §II) with 8-bit digits and one compressed histogram
  *    per digit, all digit histograms in one read pass (config c5's "multi-digit

@@ -33,7 +33,8 @@
 //
 // Choice: the MSD path is taken unless one 16-bit bin holds every key (then the
 // MSD levels would move everything for nothing and LSD skips the uniform
-// digits) — decided on the device (k_msd_plan), so nothing synchronises with
+// digits); keys sharing a prefix first move the MSD window below it
+// (k_binbits / k_keybits) — decided on the device, so nothing synchronises with
 // the host; the kernels of the path not taken return at once.
 //
 // k_scatter (the "histogram, prefix sum and stable scatter phases"):
@@ -145,6 +146,10 @@ struct MsdPlan {
   uint32_t l2_interleave;     // 1: k_scatter runs level 2 with tickets across segments (t -> r = t / 256,
                               //    s = t % 256); 0: too uneven, k_heavy runs it (level -1)
   uint32_t l2_rmax;           // most tiles in one segment
+  int32_t kb;                 // key bits the MSD path bins: key_bits, or fewer above a common prefix
+  uint32_t rehist;            // 1: the top-16 histogram is rebuilt on the window below the prefix
+  uint32_t need_keybits;      // the first histogram has one bin: k_keybits looks at the keys
+  uint64_t prefix;            // the keys' common bits above kb (0 if kb = key_bits)
   uint32_t seg_tile0[kSegs + 1];
   uint64_t seg_begin[kSegs + 1];
 };
@@ -190,7 +195,8 @@ HeavyCaps heavy_caps(uint64_t n) {
   HeavyCaps c;
   c.segs = n / (kLocalCap + 1) + 1;
   c.chunks = n / kHeavyChunkKeys + c.segs + kSegs + 1;
-  c.items = (uint64_t)kHeavyMaxLevels * (2 * (n / kLocalCap) + 2 * c.segs + 2 + n / kHeavyCopyPiece + c.segs);
+  c.items = (uint64_t)kHeavyMaxLevels * (2 * (n / kLocalCap) + 2 * c.segs + 2 + n / kHeavyCopyPiece + c.segs) +
+            kHistBins;  // + the 16-bit bins when the window moved below a common prefix
   return c;
 }
 
@@ -201,8 +207,6 @@ struct HeavyArgs {
   K* kalt;
   uint32_t* valt;
   uint64_t n;
-  int kb;      // key bits
-  int levels;  // ceil((kb - 16) / 8)
   int tma;     // every buffer 16-byte aligned: bulk-copy tiles
   HeavyCtl* ctl;
   HeavySeg* segl2;  // level -1: the first-level buckets
@@ -303,13 +307,27 @@ __global__ void __launch_bounds__(kRadix)
 // below 2^15 + 32 warps x 64 + 1024 < 65,536.
 constexpr uint32_t kHotMask = 0x80008000u;
 
-FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long long* spill, uint32_t* l1spill) {
+// bm (shared): OR / OR-of-complement of the bins that spilled (their counters
+// may read 0 at the flush although the bins are not empty).
+FS_DEVINL void mark_bin(uint32_t* bm, uint32_t bin) {
+  atomicOr(&bm[0], bin);
+  atomicOr(&bm[1], ~bin & 0xFFFFu);
+}
+
+FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long long* spill, uint32_t* l1spill,
+                       uint32_t* bm) {
   const uint32_t w = bin >> 1;
   const uint32_t old = atomicAdd(&sh[w], (bin & 1u) ? (cnt << 16) : cnt);
   if (old & kHotMask) {
     const uint32_t x = atomicExch(&sh[w], 0u);
-    if (x & 0xFFFFu) atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
-    if (x >> 16) atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
+    if (x & 0xFFFFu) {
+      atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
+      mark_bin(bm, 2 * w);
+    }
+    if (x >> 16) {
+      atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
+      mark_bin(bm, 2 * w + 1);
+    }
     if (x) atomicAdd(&l1spill[w >> 7], (x & 0xFFFFu) + (x >> 16));  // this chunk's level-1 count
   }
 }
@@ -317,16 +335,27 @@ FS_DEVINL void top_add(uint32_t* sh, uint32_t bin, uint32_t cnt, unsigned long l
 // CTA b histograms the contiguous chunk [b * chunk, (b+1) * chunk) of the keys,
 // so its flushed partial is the chunk's own 16-bit histogram: the level-1
 // scatter uses the chunks as virtual segments (k_vseg_counts / k_vseg_scan).
+//
+// First pass (msd == nullptr): the host's window [kb-16, kb).  Second pass (msd
+// != nullptr): returns at once unless k_binbits / k_keybits asked for it to be
+// rebuilt on the window below a common prefix (msd->rehist).
 template <typename K>
 __global__ void __launch_bounds__(1024, 1)
     k_top16_hist(const K* __restrict__ keys, uint64_t n, int shift, uint64_t chunk, uint32_t* __restrict__ partials,
-                 unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill) {
+                 unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill,
+                 unsigned long long* __restrict__ binbits, const MsdPlan* __restrict__ msd) {
   constexpr int kPerVec = 16 / sizeof(K);
   constexpr int kUnroll = 4;
+  if (msd != nullptr) {
+    if (!msd->rehist) return;
+    shift = msd->kb - kTopBits;
+  }
   extern __shared__ uint4 sm4[];
   uint32_t* sh = reinterpret_cast<uint32_t*>(sm4);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   uint32_t* my_l1spill = l1spill + (uint64_t)blockIdx.x * kRadix;
+  __shared__ uint32_t bm[2];
+  if (tid < 2) bm[tid] = 0;
   for (int i = tid; i < kHistWords / 4; i += 1024) sm4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
@@ -338,7 +367,7 @@ __global__ void __launch_bounds__(1024, 1)
   const uint64_t tail0 = c0 + head + nvec * kPerVec;
   for (uint64_t t = tid; t < head + (c1 - tail0); t += 1024) {  // unaligned head and ragged tail
     const uint64_t idx = t < head ? c0 + t : tail0 + (t - head);
-    top_add(sh, (uint32_t)(keys[idx] >> shift) & 0xFFFFu, 1u, spill, my_l1spill);
+    top_add(sh, (uint32_t)(keys[idx] >> shift) & 0xFFFFu, 1u, spill, my_l1spill, bm);
   }
   const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(keys + c0 + head);
   for (uint64_t it0 = 0; it0 < nvec; it0 += (uint64_t)kUnroll * 1024) {
@@ -362,16 +391,119 @@ __global__ void __launch_bounds__(1024, 1)
 #pragma unroll
       for (int j = 0; j < kPerVec; ++j) same &= b[j] == b0;
       if (__ballot_sync(kFull, same) == kFull) {  // runs (sorted / low-entropy keys): one add per warp
-        if (lane == 0) top_add(sh, b0, 32u * kPerVec, spill, my_l1spill);
+        if (lane == 0) top_add(sh, b0, 32u * kPerVec, spill, my_l1spill, bm);
       } else if (valid) {
 #pragma unroll
-        for (int j = 0; j < kPerVec; ++j) top_add(sh, b[j], 1u, spill, my_l1spill);
+        for (int j = 0; j < kPerVec; ++j) top_add(sh, b[j], 1u, spill, my_l1spill, bm);
       }
     }
   }
   __syncthreads();
   uint4* dst = reinterpret_cast<uint4*>(partials + (uint64_t)blockIdx.x * kHistWords);
   for (int i = tid; i < kHistWords / 4; i += 1024) dst[i] = sm4[i];
+  if (binbits != nullptr && tid < 2 && bm[tid]) atomicOr(&binbits[tid], (unsigned long long)bm[tid]);  // spilled bins
+}
+
+// ---- the window of the MSD path (a common prefix of the keys)
+// Bits where some keys differ decide the window: if the highest such bit hb is
+// below key_bits - 1 (the keys share a prefix) and hb + 1 >= 32, the trie bins
+// [hb - 15, hb] instead of the top 16 bits (the trie's depth only
+// spans the bits that vary) and its histogram is rebuilt there; the prefix is
+// put back on every key by the per-bin sort (k_heavy_items then sorts the
+// bins).  First the bin indices of the first histogram: OR / OR-of-complement
+// over the non-empty bins (k_binbits, whose last CTA decides); if they vary, hb
+// lies in the window; if one bin holds every key, a pass over the keys finds hb
+// (k_keybits, whose last CTA decides).  With fewer than 32 varying bits the LSD
+// path (which skips uniform digits) is taken instead.
+// Shared decision: varying bits -> the plan's window; zeroes the spills for the rebuild.
+FS_DEVINL void set_window(MsdPlan* msd, int key_bits, unsigned long long varying, unsigned long long common,
+                          unsigned long long* spill, uint32_t* l1spill, uint32_t l1spill_words, int* kb_sh) {
+  if (threadIdx.x == 0) {
+    const int kbe = varying ? 64 - __clzll((long long)varying) : 0;
+    int kb = key_bits;
+    uint64_t prefix = 0;
+    if (kbe < key_bits && kbe >= 32) {
+      kb = kbe;
+      prefix = common & ~((1ull << kbe) - 1);
+    }
+    msd->kb = kb;
+    msd->prefix = prefix;
+    msd->rehist = kb != key_bits ? 1u : 0u;
+    *kb_sh = kb;
+  }
+  __syncthreads();
+  if (*kb_sh != key_bits) {  // the second histogram pass starts from zeroed spills
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) spill[i] = 0;
+    for (uint32_t i = threadIdx.x; i < l1spill_words; i += blockDim.x) l1spill[i] = 0;
+  }
+}
+
+constexpr int kBinbitsThreads = 256;
+
+// OR / OR-of-complement of the non-empty bins over the first histogram's
+// partials (+ the bins that spilled, marked by k_top16_hist); the last CTA
+// decides the window, or asks k_keybits to look at the keys (one bin).
+__global__ void __launch_bounds__(kBinbitsThreads)
+    k_binbits(const uint32_t* __restrict__ partials, int rows, unsigned long long* __restrict__ bits,
+              uint32_t* __restrict__ done, int key_bits, MsdPlan* __restrict__ msd,
+              unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill, uint32_t l1spill_words) {
+  const uint32_t w = blockIdx.x * kBinbitsThreads + threadIdx.x;  // counter word = bins 2w, 2w + 1
+  uint32_t x = 0;
+#pragma unroll 8
+  for (int r = 0; r < rows; ++r) x |= __ldcg(partials + (uint64_t)r * kHistWords + w);
+  uint32_t o = 0, no = 0;
+  if (x & 0xFFFFu) { o |= 2 * w; no |= ~(2 * w) & 0xFFFFu; }
+  if (x >> 16) { o |= 2 * w + 1; no |= ~(2 * w + 1) & 0xFFFFu; }
+  o = __reduce_or_sync(kFull, o);
+  no = __reduce_or_sync(kFull, no);
+  if ((threadIdx.x & 31u) == 0 && (o | no)) {
+    atomicOr(&bits[0], (unsigned long long)o);
+    atomicOr(&bits[1], (unsigned long long)no);
+  }
+  __shared__ uint32_t last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ int kb_sh;
+  const unsigned long long bo = __ldcg(&bits[0]), bn = __ldcg(&bits[1]);
+  const int top = key_bits - kTopBits;
+  if (threadIdx.x == 0) msd->need_keybits = (bo & bn) ? 0u : 1u;  // one bin: look at the keys
+  set_window(msd, key_bits, (bo & bn) << top, bo << top, spill, l1spill, l1spill_words, &kb_sh);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(1024)
+    k_keybits(const K* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ bits, uint32_t* __restrict__ done,
+              int key_bits, MsdPlan* __restrict__ msd, unsigned long long* __restrict__ spill,
+              uint32_t* __restrict__ l1spill, uint32_t l1spill_words) {
+  if (!msd->need_keybits) return;
+  unsigned long long o = 0, no = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = __ldcs(keys + i);
+    o |= k;
+    no |= (K)~k;
+  }
+  const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)o), ohi = __reduce_or_sync(kFull, (uint32_t)(o >> 32));
+  const uint32_t nlo = __reduce_or_sync(kFull, (uint32_t)no), nhi = __reduce_or_sync(kFull, (uint32_t)(no >> 32));
+  if ((threadIdx.x & 31u) == 0) {
+    atomicOr(&bits[0], ((unsigned long long)ohi << 32) | olo);
+    atomicOr(&bits[1], ((unsigned long long)nhi << 32) | nlo);
+  }
+  // the last CTA to finish decides the window
+  __shared__ uint32_t last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ int kb_sh;
+  const unsigned long long mask = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1);
+  const unsigned long long ko = __ldcg(&bits[0]) & mask, kn = __ldcg(&bits[1]) & mask;
+  set_window(msd, key_bits, ko & kn, ko, spill, l1spill, l1spill_words, &kb_sh);
 }
 
 // Level-1 digit counts of every chunk: cnt[v][d] = sum of the chunk's 256 leaves
@@ -417,11 +549,12 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kSegs)
     k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
                MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
-               HeavySeg* __restrict__ hl2) {
+               HeavySeg* __restrict__ hl2, HeavyItem* __restrict__ hitems) {
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
   __shared__ int one_bin;
   const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
+  const uint32_t rehist = plan->rehist;
   if (s == 0) {
     one_bin = 0;
     rmax = 0;
@@ -433,6 +566,14 @@ __global__ void __launch_bounds__(kSegs)
     const uint64_t c = __ldg(H16 + v);
     if (c == n) one_bin = 1;
     if (c > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{P16[v], c, 0, 0, 0, 0};
+  }
+  if (rehist) {  // shifted window: the bins are sorted as items (see k_local_sort)
+    const uint32_t R = (uint32_t)(plan->kb - kTopBits);
+    for (int j = 0; j < kHistBins / kSegs; ++j) {
+      const uint32_t v = j * kSegs + s;
+      const uint64_t c = H16[v];
+      if (c > 1 && c <= (uint64_t)kLocalCap) hitems[atomicAdd(&hctl->nitems, 1u)] = HeavyItem{P16[v], c, R, (uint16_t)R, 0};
+    }
   }
   const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
   const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
@@ -661,7 +802,7 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
   }
   __syncthreads();
 
-  const int shift = a.shift;
+  const int shift = a.mode == 0 ? a.shift : a.msd->kb - kRadixBits * a.mode;  // MSD: the plan's window
 #ifdef FS_SCATTER_STATS
   long long ph_t0 = clock64();
 #endif
@@ -1149,11 +1290,14 @@ template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(kLocalThreads, 2)
     k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
                  const MsdPlan* __restrict__ msd) {
-  if (!msd->use_msd) return;
+  // (R is the host's key_bits - 16.  A window moved below a common prefix sends
+  // every bin to k_heavy_items instead: a loaded R costs ~26 us here at c5 — it
+  // takes a register where the kernel parameter is an operand.)
   const uint32_t bkt = blockIdx.x;
+  const uint32_t use = __ldg(&msd->use_msd), rehist = __ldg(&msd->rehist);
   const uint64_t b0 = __ldg(P16 + bkt);
   const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
-  if (m <= 1 || m > (uint32_t)kLocalCap) return;
+  if (!use || rehist || m <= 1 || m > (uint32_t)kLocalCap) return;
   sort_bin<K, kHasValues>(keys, vals, keys, vals, b0, m, R, (K)((uint64_t)bkt << R));
 }
 
@@ -1162,7 +1306,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 // ================================================================ driver
 struct WideLayout {
   size_t alt_k = 0, alt_v = 0, partials = 0;
-  size_t zero_begin = 0, spill = 0, l1spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0,
+  size_t zero_begin = 0, kbits = 0, spill = 0, l1spill = 0, scan_status = 0, tickets = 0, digit_hist = 0, status = 0,
          zero_end = 0;
   size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
   size_t hctl = 0, hseg0 = 0, hseg1 = 0, hsegl2 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // k_heavy
@@ -1194,6 +1338,8 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   L.partials = off;
   if (L.use_msd) off = align_up(off + (size_t)L.hgrid * kHistWords * 4);
   L.zero_begin = off;  // zeroed by one memset per call
+  L.kbits = off;  // OR / OR-of-complement of the non-empty bins, then of the keys (the window)
+  if (L.use_msd) off = align_up(off + 5 * sizeof(unsigned long long));  // + the k_keybits done counter
   L.spill = off;
   if (L.use_msd) off = align_up(off + sizeof(unsigned long long) * kHistBins);
   L.l1spill = off;
@@ -1293,15 +1439,27 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
       return e;
     auto* l1spill = (uint32_t*)(t + L.l1spill);
     auto* vcnt = (uint32_t*)(t + L.vcnt);
+    auto* kbits = (unsigned long long*)(t + L.kbits);
+    const uint32_t l1w = (uint32_t)(kRadix * L.hgrid);
     k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
-                                                 l1spill);
+                                                 l1spill, kbits, nullptr);
+    // the window (a common prefix): a decision from the bins, a pass over the
+    // keys only if one bin holds them all, and the histogram again only if the
+    // window moved (each kernel returns at once otherwise)
+    k_binbits<<<kHistWords / kBinbitsThreads, kBinbitsThreads, 0, s>>>(partials, L.hgrid, kbits,
+                                                                        (uint32_t*)(kbits + 4), key_bits, msd,
+                                                                        spill, l1spill, l1w);
+    k_keybits<K><<<(unsigned)sms, 1024, 0, s>>>(kin, n, kbits + 2, (uint32_t*)(kbits + 4) + 1, key_bits, msd, spill,
+                                                l1spill, l1w);
+    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
+                                                 l1spill, nullptr, msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_merge_scan(partials, L.hgrid, spill, nullptr, kHistBins, H16, kHistBins, 0, P16, scan_status,
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
     auto* hctl = (HeavyCtl*)(t + L.hctl);
     k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0),
-                                   (HeavySeg*)(t + L.hsegl2));
+                                   (HeavySeg*)(t + L.hsegl2), (HeavyItem*)(t + L.hitems));
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1321,8 +1479,6 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     HeavyArgs<K> ha{};
     ha.kout = kout; ha.vout = vout; ha.kalt = alt_k; ha.valt = alt_v;
     ha.n = n;
-    ha.kb = key_bits;
-    ha.levels = (key_bits - kTopBits + kRadixBits - 1) / kRadixBits;
     ha.tma = tma ? 1 : 0;
     ha.ctl = hctl;
     ha.segl2 = (HeavySeg*)(t + L.hsegl2);

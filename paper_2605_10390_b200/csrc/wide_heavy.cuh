@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
   uint32_t par = 0;           // bit b: parity of the next phase of buffer b's mbarrier (uniform over the CTA)
   uint32_t nb = 0;            // buffer of the next tile
 
-  for (int level = -1; level < a.levels; ++level) {
+  const int kb = a.msd->kb;  // the plan's window (below a common prefix, if any)
+  const int levels = (kb - kTopBits + kRadixBits - 1) / kRadixBits;
+  for (int level = -1; level < levels; ++level) {
     const bool l2 = level < 0;  // the uneven level-2 pass
     const int cur = level & 1;
     HeavySeg* segs = l2 ? a.segl2 : (cur ? a.seg1 : a.seg0);
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
       return;  // same value in every CTA (written before the last grid barrier)
     }
     const int slot = level + 1;
-    const int rem = a.kb - kTopBits - kRadixBits * level;  // bits below the digits done so far
+    const int rem = kb - kTopBits - kRadixBits * level;  // bits below the digits done so far
     const int w = rem < kRadixBits ? rem : kRadixBits;
     const int sh = rem - w;
     const uint32_t dmask = (1u << w) - 1u;

@@ -30,13 +30,16 @@ def make(kind):
     elif kind == "hot1x50":  # half the keys in one bin
         hot = (ri & 1) == 0
         ki[:] = torch.where(hot, (0x7777 << 48) | low48, ki)
+    elif kind.startswith("lt2^"):  # a common zero prefix: keys < 2^b
+        b = int(kind[4:])
+        ki[:] = ki & ((1 << b) - 1)
     elif kind == "clustered":  # 64 clusters, each 2^-8 wide in the key space (about 256 bins each)
         c = (ri & 63) * 0x0400_0000_0000_0000 // 1
         ki[:] = (c + (ki & ((1 << 56) - 1)))
     return k
 
 
-kinds = ["uniform", "hot16x25", "hot1x50", "clustered"]
+kinds = sys.argv[2].split(",") if len(sys.argv) > 2 else ["uniform", "hot16x25", "hot1x50", "clustered", "lt2^56", "lt2^48", "lt2^40"]
 libs = sorted(glob.glob(os.path.join(ROOT, "scripts/microbench/variants/*.so"))) or \
     [os.path.join(ROOT, "paper_2605_10390_b200/libfractalsort.so")]
 for path in libs:

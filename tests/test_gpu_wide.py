@@ -253,11 +253,33 @@ def test_msd_recursion_many_small_oversize_bins(cuda):
     _check_pairs(cuda, k)
 
 
-def test_msd_common_prefix_takes_lsd(cuda):
-    """Every key in one 16-bit bin (a common prefix): the device takes the LSD
-    path, which skips the uniform digits."""
+@pytest.mark.parametrize("prefix,free_bits", [(0, 40), (0xABCDEF, 40), (0, 32), (0x5A, 56), (1, 63)])
+def test_msd_common_prefix_window(cuda, prefix, free_bits):
+    """Keys sharing their bits above `free_bits` (a common prefix, zero or not):
+    the MSD path bins the 16 bits below the prefix (a rebuilt trie histogram)
+    and puts the prefix back on every key."""
     n = (1 << 22) + 5
-    k = datagen.gen_u64(n, seed=80) & np.uint64((1 << 40) - 1)
+    k = datagen.gen_u64(n, seed=80 + free_bits) & np.uint64((1 << free_bits) - 1)
+    k |= np.uint64(prefix) << np.uint64(free_bits)
+    _check_pairs(cuda, k)
+
+
+def test_msd_common_prefix_with_oversize_bins(cuda):
+    """A common prefix and, below it, oversize bins: the recursion runs on the
+    shifted window."""
+    n = (1 << 22) + 5
+    k = datagen.gen_u64(n, seed=85) & np.uint64((1 << 44) - 1)
+    hot = datagen.gen_u64(n, seed=86) % np.uint64(4) == 0
+    k[hot] = (k[hot] & np.uint64((1 << 28) - 1)) | np.uint64(0xBEE << 28)
+    k |= np.uint64(0x77) << np.uint64(48)
+    _check_pairs(cuda, k)
+
+
+def test_msd_narrow_effective_keys_take_lsd(cuda):
+    """Fewer than 32 varying bits under key_bits = 64: the LSD path (uniform
+    digits skipped)."""
+    n = (1 << 22) + 5
+    k = datagen.gen_u64(n, seed=87) & np.uint64((1 << 24) - 1)
     _check_pairs(cuda, k)
 
 
