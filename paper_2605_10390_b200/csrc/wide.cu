@@ -143,8 +143,8 @@ struct LsdPlan {
 struct MsdPlan {
   uint32_t use_msd;           // 1: MSD kernels run, LSD kernels return; 0: the reverse
   uint32_t l2_tiles;          // tiles of the level-2 pass
-  uint32_t l2_interleave;     // 1: k_scatter runs level 2 with tickets across segments (t -> r = t / 256,
-                              //    s = t % 256); 0: too uneven, k_heavy runs it (level -1)
+  uint32_t l2_interleave;     // 1 (level 2 always interleaves: t -> r = t / 256, s = t % 256; buckets too
+                              //    large for the status rows have 0 tiles here and run in k_heavy, level -1)
   uint32_t l2_rmax;           // most tiles in one segment
   int32_t kb;                 // key bits the MSD path bins: key_bits, or fewer above a common prefix
   uint32_t rehist;            // 1: the top-16 histogram is rebuilt on the window below the prefix
@@ -575,8 +575,20 @@ __global__ void __launch_bounds__(kSegs)
       if (c > 1 && c <= (uint64_t)kLocalCap) hitems[atomicAdd(&hctl->nitems, 1u)] = HeavyItem{P16[v], c, R, (uint16_t)R, 0};
     }
   }
+  // Level 2: interleaved tickets (k_scatter mode 2) keep every bucket's lookback
+  // one tile deep, but cost 256 x (most tiles in one bucket) status rows.  A
+  // bucket above status_cap / 256 tiles (about 1.25x the mean) is left out of
+  // the interleave (its tickets are holes) and run by k_heavy instead (chunk
+  // histograms, CTA-owned chunks, no lookback).
   const uint64_t b = P16[s * 256], e = P16[(s + 1) * 256];
-  const uint32_t tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
+  const uint32_t all_tiles = (uint32_t)((e - b + kSTile - 1) / kSTile);
+#ifdef FS_FORCE_L2_HEAVY  // timing experiment: level 2 always in k_heavy
+  const bool to_heavy = e > b && status_cap;
+#else
+  const bool to_heavy = (uint64_t)all_tiles * kSegs > (uint64_t)status_cap;
+#endif
+  const uint32_t tiles = to_heavy ? 0u : all_tiles;
+  if (to_heavy) hl2[atomicAdd(&hctl->nl2, 1u)] = HeavySeg{b, e - b, 0, 0, 1, 0};
   atomicMax(&rmax, tiles);
   const uint32_t inc = warp_inclusive_scan<uint32_t>(tiles);
   if (lane == 31) wsum[warp] = inc;
@@ -595,20 +607,11 @@ __global__ void __launch_bounds__(kSegs)
     plan->l2_tiles = tot;
   }
   __syncthreads();
-  // Interleaved tickets keep every segment's lookback one tile deep; worth it
-  // unless the segments are so uneven that most tickets would be holes: then
-  // k_heavy runs level 2 over the buckets as segments (chunk histograms, no lookback).
-#ifdef FS_FORCE_L2_HEAVY  // timing experiment: level 2 always in k_heavy
-  const bool inter = false && status_cap;
-#else
-  const bool inter = (uint64_t)rmax * kSegs <= (uint64_t)status_cap;
-#endif
   if (s == 0) {
     plan->use_msd = one_bin ? 0u : 1u;
     plan->l2_rmax = rmax;
-    plan->l2_interleave = inter ? 1u : 0u;
+    plan->l2_interleave = 1u;
   }
-  if (!inter && e > b) hl2[atomicAdd(&hctl->nl2, 1u)] = HeavySeg{b, e - b, 0, 0, 1, 0};
 }
 
 // ================================================================ scatter pass
@@ -698,7 +701,6 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
       inter = true;
       ntiles = a.l1_nseg * a.l1_chunk_tiles;
     } else {
-      if (!a.msd->l2_interleave) return;  // uneven buckets: k_heavy runs this level
       src_k = a.kB; src_v = a.vB; dst_k = a.kA; dst_v = a.vA;
       base_tab = a.P16;
       base_ss = 256;  // level 2: base[s][d] = P16[(s << 8) | d]
