@@ -80,8 +80,19 @@ constexpr int kMaxGrid = 1024;              // CTAs (one per SM): the merge loop
 constexpr int kSmallGrid = 32;              // up to this many CTAs, the merge of stage 1b is column-per-thread
 static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violated");
 
+#ifndef FS_HIST_HOT
+#define FS_HIST_HOT 1
+#endif
+#ifndef FS_HIST_HOT_ALWAYS
+#define FS_HIST_HOT_ALWAYS 0
+#endif
+// The CTA's hot key (skewed inputs): the first key whose counter crossed 2^15
+// (0xFFFFFFFF: none yet).  Warps that see it count that key in registers.
+__shared__ uint32_t s_hot_key;
+
 FS_DEVINL void spill_word(uint32_t* sh, uint32_t w, unsigned long long* spill) {
   const uint32_t x = atomicExch(&sh[w], 0u);
+  if (FS_HIST_HOT) atomicCAS(&s_hot_key, 0xFFFFFFFFu, (x & 0xFFFFu) >= (x >> 16) ? 2 * w : 2 * w + 1);
   if (x & 0xFFFFu) atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
   if (x >> 16) atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
 }
@@ -105,6 +116,23 @@ FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
     const uint32_t x = w[j];
     acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
     acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
+  }
+  return acc;
+}
+
+// add8 for skewed inputs: keys equal to the hot key `h` are counted in a
+// register (hc) instead of contending for one shared-memory word.
+FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  char* base = reinterpret_cast<char*>(sh);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t x = w[j];
+    if ((x & 0xFFFFu) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
+    else ++hc;
+    if ((x >> 16) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
+    else ++hc;
   }
   return acc;
 }
@@ -174,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
 #pragma unroll
   for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
   for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins + 1; i += gridDim.x * kThreads) a.spill[i] = 0;
+  if (tid == 0) s_hot_key = 0xFFFFFFFFu;
   grid.sync();
   FS_TRACE(1);
 
@@ -207,9 +236,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   const uint64_t nstatic = ngroups - ngroups / FS_HIST_DYN_DIV;
   bool agg = false;
   uint32_t phase = 0;
+  uint32_t hot = 0xFFFFFFFFu, hot_cnt = 0;  // this warp's view of s_hot_key, refreshed every 4th group
   // the whole warp calls this together (warp votes inside)
   auto process_v = [&](uint4 (&v)[kUnroll]) {
     if (agg || phase == 0) {
+      if (FS_HIST_HOT) hot = s_hot_key;  // one broadcast load: warp-uniform
       bool runs = false;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) runs |= all8_equal(v[u]);
@@ -221,8 +252,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
       for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill);
     } else {
       uint32_t acc = 0;
+      if (FS_HIST_HOT && (FS_HIST_HOT_ALWAYS || hot != 0xFFFFFFFFu)) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc |= add8(sh, v[u]);
+        for (int u = 0; u < kUnroll; ++u) acc |= add8_hot(sh, v[u], hot, hot_cnt);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) acc |= add8(sh, v[u]);
+      }
       if (acc & kHotMask) {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) recheck8(sh, v[u], a.spill);
@@ -272,6 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
         for (int u = 0; u < kUnroll; ++u) cur[u] = nxt[u];
       }
     }
+  }
+  if (FS_HIST_HOT && hot != 0xFFFFFFFFu) {  // keys counted in registers: added to the global spill once
+    const uint32_t t = warp_sum(hot_cnt);
+    if (lane_id() == 0 && t) atomicAdd(&a.spill[hot], (unsigned long long)t);
   }
   // Vectors after the last full group (< 2,048).
   for (uint64_t i = ngroups * kGroupVec + (uint64_t)blockIdx.x * kThreads + tid; i < nvec;

@@ -58,6 +58,31 @@ def test_sort_u16_two_hot_bins(cuda):
     np.testing.assert_array_equal(out, oracle.sort_u16(keys))
 
 
+@pytest.mark.parametrize("hot,frac", [(0xFFFF, 0.5), (0, 0.6), (0x1235, 0.05)])
+def test_sort_u16_hot_key(cuda, hot, frac):
+    """One key far above the others (a CTA's first spill makes it the warps'
+    register-counted hot key): bins at both ends of the table, and a key just
+    hot enough to spill in some CTAs only."""
+    n = (1 << 24) + 3
+    k = datagen.gen_u16("uniform", n, seed=7)
+    sel = datagen.gen_u16("uniform", n, seed=8).astype(np.float64) / 65536.0 < frac
+    k[sel] = hot
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), oracle.sort_u16(k))
+    np.testing.assert_array_equal(to_host(fs.histogram_u16(to_dev(k, cuda))).astype(np.uint64), oracle.histogram_u16(k))
+
+
+def test_sort_u16_hot_key_changes(cuda):
+    """The hot key changes halfway (key A, then key B): the CTA keeps its first
+    hot key; B's counts go through the shared-memory counters and their spill."""
+    n = (1 << 24) + 1
+    k = datagen.gen_u16("uniform", n, seed=9)
+    sel = datagen.gen_u16("uniform", n, seed=10) < 40000
+    half = np.arange(n) < n // 2
+    k[sel & half] = 0x0A0A
+    k[sel & ~half] = 0xB0B0
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), oracle.sort_u16(k))
+
+
 @pytest.mark.parametrize("offset", range(8))
 def test_sort_u16_misaligned(cuda, offset):
     """Input and output start at every 2-byte offset of a 16-byte vector."""
