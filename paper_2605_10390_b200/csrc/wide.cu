@@ -117,6 +117,9 @@ constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 // ---- MSD geometry
 constexpr int kTopBits = 16;            // bits binned by the trie (two 8-bit MSD levels)
 constexpr int kSegs = 256;              // first-level segments
+#ifndef FS_LOCAL_REHIST_INLINE
+#define FS_LOCAL_REHIST_INLINE 0
+#endif
 #ifndef FS_LOCAL_THREADS
 #define FS_LOCAL_THREADS 512
 #endif
@@ -172,10 +175,9 @@ struct HeavySeg {
 
 struct HeavyItem {
   uint64_t begin, count;
-  uint32_t R;    // keys lie in [top, top + 2^R), top = first key with its low `sh` bits cleared;
-                 // sorted by key - top (0: already in order, copy only)
-  uint16_t sh;
-  uint16_t buf;  // where the keys lie
+  uint64_t top;  // every key lies in [top, top + 2^R); sorted by key - top
+  uint32_t R;    // 0: already in order, copy only
+  uint32_t buf;  // where the keys lie
 };
 constexpr uint64_t kHeavyCopyPiece = 1ull << 20;  // copy items are emitted in pieces of this many keys
 
@@ -481,10 +483,31 @@ __global__ void __launch_bounds__(1024)
               uint32_t* __restrict__ l1spill, uint32_t l1spill_words) {
   if (!msd->need_keybits) return;
   unsigned long long o = 0, no = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const K k = __ldcs(keys + i);
+  constexpr int kPerVec = 16 / sizeof(K);
+  const uint64_t head0 = ((16 - ((uintptr_t)keys & 15)) & 15) / sizeof(K), head = head0 < n ? head0 : n;
+  const uint64_t nvec = (n - head) / kPerVec, tail0 = head + nvec * kPerVec;
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = gt; i < head + (n - tail0); i += gs) {  // unaligned head and ragged tail
+    const K k = keys[i < head ? i : tail0 + (i - head)];
     o |= k;
     no |= (K)~k;
+  }
+  const uint4* vec = reinterpret_cast<const uint4*>(keys + head);
+  uint32_t oA = 0, oB = 0, nA = 0, nB = 0;  // word-wise: x, z = u64 low halves (u32: keys), y, w = high halves
+#pragma unroll 4
+  for (uint64_t i = gt; i < nvec; i += gs) {
+    const uint4 q = ld_stream_v4(vec + i);
+    oA |= q.x | q.z;
+    oB |= q.y | q.w;
+    nA |= ~q.x | ~q.z;
+    nB |= ~q.y | ~q.w;
+  }
+  if (sizeof(K) == 8) {
+    o |= ((unsigned long long)oB << 32) | oA;
+    no |= ((unsigned long long)nB << 32) | nA;
+  } else {
+    o |= oA | oB;
+    no |= nA | nB;
   }
   const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)o), ohi = __reduce_or_sync(kFull, (uint32_t)(o >> 32));
   const uint32_t nlo = __reduce_or_sync(kFull, (uint32_t)no), nhi = __reduce_or_sync(kFull, (uint32_t)(no >> 32));
@@ -572,7 +595,8 @@ __global__ void __launch_bounds__(kSegs)
     for (int j = 0; j < kHistBins / kSegs; ++j) {
       const uint32_t v = j * kSegs + s;
       const uint64_t c = H16[v];
-      if (c > 1 && c <= (uint64_t)kLocalCap) hitems[atomicAdd(&hctl->nitems, 1u)] = HeavyItem{P16[v], c, R, (uint16_t)R, 0};
+      if (!FS_LOCAL_REHIST_INLINE && c > 1 && c <= (uint64_t)kLocalCap)
+        hitems[atomicAdd(&hctl->nitems, 1u)] = HeavyItem{P16[v], c, plan->prefix | ((uint64_t)v << R), R, 0};
     }
   }
   // Level 2: interleaved tickets (k_scatter mode 2) keep every bucket's lookback
@@ -1299,7 +1323,16 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   const uint32_t use = __ldg(&msd->use_msd), rehist = __ldg(&msd->rehist);
   const uint64_t b0 = __ldg(P16 + bkt);
   const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
-  if (!use || rehist || m <= 1 || m > (uint32_t)kLocalCap) return;
+  if (!use || m <= 1 || m > (uint32_t)kLocalCap) return;
+#if FS_LOCAL_REHIST_INLINE
+  if (rehist) {  // the window moved below a common prefix: the plan's R and prefix
+    const int Rw = __ldg(&msd->kb) - kTopBits;
+    sort_bin<K, kHasValues>(keys, vals, keys, vals, b0, m, Rw, (K)(__ldg(&msd->prefix) | ((uint64_t)bkt << Rw)));
+    return;
+  }
+#else
+  if (rehist) return;
+#endif
   sort_bin<K, kHasValues>(keys, vals, keys, vals, b0, m, R, (K)((uint64_t)bkt << R));
 }
 

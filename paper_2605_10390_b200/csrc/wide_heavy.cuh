@@ -70,7 +70,7 @@ FS_DEVINL HeavySeg load_seg(const HeavySeg* p) {
 // Copy items for [b, b + cnt) of the temporary buffer, in pieces.
 FS_DEVINL void emit_copy(HeavyCtl* ctl, HeavyItem* items, uint64_t b, uint64_t cnt) {
   for (uint64_t o = 0; o < cnt; o += kHeavyCopyPiece)
-    items[atomicAdd(&ctl->nitems, 1u)] = HeavyItem{b + o, min(kHeavyCopyPiece, cnt - o), 0u, 0, 1};
+    items[atomicAdd(&ctl->nitems, 1u)] = HeavyItem{b + o, min(kHeavyCopyPiece, cnt - o), 0ull, 0u, 1u};
 }
 
 // Block-wide exclusive scan over the 256 threads (one value each).
@@ -204,17 +204,21 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
         if (final_level) {  // after this scatter the segment is sorted
           if (dbuf) emit_copy(a.ctl, a.items, sg.begin, sg.count);
         } else {
+          // the segment's common bits above the digit (every key shares them)
+          const K* src = sg.buf ? a.kalt : a.kout;
+          const uint64_t key0 = (uint64_t)__ldcg(src + sg.begin);
+          const uint64_t common = sh + w >= 64 ? 0ull : key0 & ~((1ull << (sh + w)) - 1);
           uint64_t pos = sg.begin, ib = 0;
           uint32_t isz = 0, d0 = 0, d1 = 0;
           // An item spanning digits d0..d1 holds keys in [top, top + (d1 - d0 + 1) << sh)
-          // with top = its first key's bits above sh: sorted by ceil(log2(span)) + sh bits,
-          // so a merged item's counting digit is not spent on the few digits it spans.
+          // with top = common | d0 << sh: sorted by ceil(log2(span)) + sh bits, so a
+          // merged item's counting digit is not spent on the few digits it spans.
           auto close = [&]() {
             if (isz > 0) {
               const uint32_t span = d1 - d0 + 1;
               const uint32_t lg = span > 1 ? 32 - __clz(span - 1) : 0;
               a.items[atomicAdd(&a.ctl->nitems, 1u)] =
-                  HeavyItem{ib, isz, (uint32_t)sh + lg, (uint16_t)sh, (uint16_t)dbuf};
+                  HeavyItem{ib, isz, common | ((uint64_t)d0 << sh), (uint32_t)sh + lg, dbuf};
             }
             isz = 0;
           };
@@ -378,8 +382,11 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
                   const HeavyItem* __restrict__ items, const MsdPlan* __restrict__ msd) {
   if (!msd->use_msd) return;
   const uint32_t ni = ctl->nitems;
+  HeavyItem nxt;
+  if (blockIdx.x < ni) nxt = items[blockIdx.x];
   for (uint32_t it = blockIdx.x; it < ni; it += gridDim.x) {
-    const HeavyItem item = items[it];
+    const HeavyItem item = nxt;
+    if (it + gridDim.x < ni) nxt = items[it + gridDim.x];  // in flight during this item's sort
     const K* sk = item.buf ? kalt : kout;
     const uint32_t* sv = item.buf ? valt : vout;
     if (item.R == 0 || item.count <= 1) {
@@ -389,8 +396,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
           if (kHasValues) vout[item.begin + j] = sv[item.begin + j];
         }
     } else {
-      const K top = sk[item.begin] & (K)~((1ull << item.sh) - 1);
-      sort_bin<K, kHasValues>(sk, sv, kout, vout, item.begin, (uint32_t)item.count, (int)item.R, top);
+      sort_bin<K, kHasValues>(sk, sv, kout, vout, item.begin, (uint32_t)item.count, (int)item.R, (K)item.top);
     }
     __syncthreads();  // the shared memory of sort_bin is reused by the next item
   }
