@@ -18,5 +18,5 @@ NB="--no-e2e --no-cpu-baseline --no-verify"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 5 --warmup 3 $NB > $O/ncu_launch_c2.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c5.csv python bench.py --workload c5 --steps 2 --warmup 1 $NB > $O/ncu_launch_c5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_hist16|k_expand16" -s 4 -c 2 -o $O/prof_c2 -f python bench.py --steps 3 --warmup 3 $NB > $O/ncu_full_c2.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_top16_hist|k_scatter|k_local_sort" -c 4 -o $O/prof_c5 -f python bench.py --workload c5 --steps 1 --warmup 0 $NB > $O/ncu_full_c5.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_top16_hist|k_scatter|k_local_sort" -c 5 -o $O/prof_c5 -f python bench.py --workload c5 --steps 1 --warmup 0 $NB > $O/ncu_full_c5.log 2>&1
 ls -la $O
