@@ -92,7 +92,9 @@ U16Layout u16_layout(uint64_t n, bool with_prefix) {
   L.slice_tot_off = off;
   off = align_up(off + sizeof(uint64_t) * kHistSlices);
   L.partials_off = off;
-  off = align_up(off + sizeof(uint32_t) * kHistWords * (size_t)L.grid);
+  // the one-cluster sort (small16.cu) needs 16 partial rows whatever n
+  const size_t rows = (with_prefix && n <= small16_max_n() && L.grid < 16) ? 16 : (size_t)L.grid;
+  off = align_up(off + sizeof(uint32_t) * kHistWords * rows);
   L.prefix_off = off;
   if (with_prefix) off = align_up(off + sizeof(uint64_t) * (kHistBins + 1));
   L.total = off;
@@ -168,6 +170,13 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
   phase_event(0, s);
   phase_event(1, s);
   cudaError_t e;
+  if (n <= small16_max_n()) {  // one cluster launch: every stage on chip
+    if ((e = launch_sort16_small(keys_in, n, keys_out, spill, partials, s)) != cudaSuccess)
+      return cuda_fail(e, "fs_sort_keys_u16: sort16_small (one-cluster sort)");
+    phase_event(2, s);
+    phase_event(3, s);
+    return finish(s, "fs_sort_keys_u16");
+  }
   if ((e = launch_hist16(keys_in, n, partials, spill, nullptr, 0, 0, prefix, slice_tot, L.grid, s)) !=
       cudaSuccess)
     return cuda_fail(e, "fs_sort_keys_u16: hist16 (histogram + merge + scan)");

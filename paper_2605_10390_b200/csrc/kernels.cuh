@@ -31,6 +31,15 @@ cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, 
                           uint64_t* hist_out, uint64_t nbins_out, int accumulate, uint64_t* prefix,
                           uint64_t* slice_tot, int grid, cudaStream_t s);
 
+// ---------------------------------------------------------------- small16.cu
+// The whole u16 keys-only sort in one launch of a 16-CTA cluster for n <=
+// small16_max_n() (histogram in shared memory, merge of the 16 tables through
+// L2, scan, expansion).  spill: 65,536 u64 of scratch (zeroed by the kernel);
+// partials: 16 x kHistWords u32 of scratch.
+uint64_t small16_max_n();
+cudaError_t launch_sort16_small(const uint16_t* keys, uint64_t n, uint16_t* out, unsigned long long* spill,
+                                uint32_t* partials, cudaStream_t s);
+
 // ---------------------------------------------------------------- scan.cu
 constexpr int kScanTileBins = 256;
 inline uint64_t scan_tiles(uint64_t nbins) { return (nbins + kScanTileBins - 1) / kScanTileBins; }

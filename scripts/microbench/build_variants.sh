@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")/../.."
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-SRCS="abi hist16 scan expand16 wide partition host_stream trie peer"
+SRCS="abi hist16 scan expand16 wide partition host_stream trie peer small16"
 mkdir -p scripts/microbench/variants
 for spec in "$@"; do
   name="${spec%%:*}"; defs="${spec#*:}"

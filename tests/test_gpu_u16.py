@@ -58,6 +58,26 @@ def test_sort_u16_two_hot_bins(cuda):
     np.testing.assert_array_equal(out, oracle.sort_u16(keys))
 
 
+@pytest.mark.parametrize("n", [1, 9, 4095, 65536, 100_003, (1 << 18) - 1, 1 << 18, (1 << 18) + 1])
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "const", "sortedswap"])
+def test_sort_u16_one_cluster_path(cuda, n, dist):
+    """Sizes up to 2^18 take the one-launch cluster sort (small16.cu); the
+    boundary and just above it take the two-kernel path."""
+    k = datagen.gen_u16(dist, n, seed=n % 97)
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), oracle.sort_u16(k))
+
+
+@pytest.mark.parametrize("offset", [1, 3, 7])
+def test_sort_u16_one_cluster_misaligned_in_place(cuda, offset):
+    """The cluster sort with keys and output not 16-byte aligned (scalar loads
+    and stores), in place."""
+    n = 200_001
+    k = datagen.gen_u16("uniform", n + offset, seed=offset)
+    d = to_dev(k, cuda)[offset:]
+    fs.sort_keys(d, out=d)
+    np.testing.assert_array_equal(to_host(d), oracle.sort_u16(k[offset:]))
+
+
 @pytest.mark.parametrize("hot,frac", [(0xFFFF, 0.5), (0, 0.6), (0x1235, 0.05)])
 def test_sort_u16_hot_key(cuda, hot, frac):
     """One key far above the others (a CTA's first spill makes it the warps'
