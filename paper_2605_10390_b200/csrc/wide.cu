@@ -3,7 +3,7 @@
 //
 // Two bit-identical schemes (the stable sort is unique, ledger 28):
 //
-// (1) Trie-binned MSD (default for n >= 2^22 and key_bits >= 32).  The paper's
+// (1) Trie-binned MSD (default for n >= 2^18 and key_bits >= 32).  The paper's
 //     high-precision path (§III.G.3, Alg. 5) bins the keys by
 //     the top levels of the compressed trie and then sorts each bin by its
 //     remaining bits (per-bin radix), with the index array I
@@ -134,7 +134,16 @@ static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
 constexpr int kCountBitsMax = FS_LOCAL_CB;  // local counting digit (<= 4,096 groups)
 constexpr int kRankU = 4;              // keys ranked at once per thread (ILP)
 constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
-constexpr uint64_t kMsdMinN = 1ull << 22;
+#ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
+#define FS_TINY_MAX 128
+#endif
+#ifndef FS_MSD_MIN_N
+#define FS_MSD_MIN_N (1ull << 18)  // below: LSD (65,536 keys: 244 us vs 274 for MSD)
+#endif
+constexpr uint64_t kMsdMinN = FS_MSD_MIN_N;
+constexpr uint32_t kTinyMax = FS_TINY_MAX;
+constexpr uint64_t kListBigMaxN = 1ull << 26;  // below: k_local_sort runs from the plan's list of bins
+  // bins of <= 64 keys: one warp each (k_tiny_bins), not a CTA
 
 struct LsdPlan {
   uint64_t base[kMaxPasses][kRadix];  // exclusive digit offsets
@@ -187,6 +196,8 @@ struct HeavyCtl {
   uint32_t nchunks[kHeavyMaxLevels + 1];    // per level + 1
   uint32_t ticket[kHeavyMaxLevels + 1];
   uint32_t nitems;
+  uint32_t ntiny;                           // bins of 2..kTinyMax keys (k_tiny_bins)
+  uint32_t nbig;                            // bins for k_local_sort when it runs from a list (small inputs)
 };
 
 struct HeavyCaps {
@@ -572,7 +583,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kSegs)
     k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
                MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
-               HeavySeg* __restrict__ hl2, HeavyItem* __restrict__ hitems) {
+               HeavySeg* __restrict__ hl2, HeavyItem* __restrict__ hitems, uint32_t* __restrict__ tiny,
+               uint32_t* __restrict__ big, int list_big) {
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
   __shared__ int one_bin;
@@ -583,12 +595,53 @@ __global__ void __launch_bounds__(kSegs)
     rmax = 0;
   }
   __syncthreads();
+  uint32_t tiny_bits[kHistBins / kSegs / 32] = {};  // bins of 2..kTinyMax keys (bit j: bin j * 256 + s)
+  uint32_t big_bits[kHistBins / kSegs / 32] = {};   // bins for k_local_sort (listed only for small inputs)
 #pragma unroll 16
   for (int j = 0; j < kHistBins / kSegs; ++j) {  // coalesced, 16 loads in flight per thread
     const uint32_t v = j * kSegs + s;
     const uint64_t c = __ldg(H16 + v);
     if (c == n) one_bin = 1;
     if (c > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{P16[v], c, 0, 0, 0, 0};
+    if (c >= 2 && c <= kTinyMax) tiny_bits[j >> 5] |= 1u << (j & 31);
+    if (list_big && c > kTinyMax && c <= (uint64_t)kLocalCap) big_bits[j >> 5] |= 1u << (j & 31);
+  }
+  {  // lists of the tiny bins (2..kTinyMax keys) and, for small inputs, of the
+     // others the local sort takes: offsets by a block scan (no atomics)
+    __shared__ uint32_t lsum[2][kSegs / 32];
+    uint32_t nt = 0, nb = 0;
+#pragma unroll
+    for (int q = 0; q < kHistBins / kSegs / 32; ++q) {
+      nt += __popc(tiny_bits[q]);
+      nb += __popc(big_bits[q]);
+    }
+    const uint32_t it = warp_inclusive_scan<uint32_t>(nt), ib = warp_inclusive_scan<uint32_t>(nb);
+    if (lane == 31) {
+      lsum[0][warp] = it;
+      lsum[1][warp] = ib;
+    }
+    __syncthreads();
+    uint32_t ot = it - nt, ob = ib - nb, tt = 0, tb = 0;
+#pragma unroll
+    for (int w = 0; w < kSegs / 32; ++w) {
+      if (w < (int)warp) {
+        ot += lsum[0][w];
+        ob += lsum[1][w];
+      }
+      tt += lsum[0][w];
+      tb += lsum[1][w];
+    }
+    if (s == 0) {
+      hctl->ntiny = rehist ? 0u : tt;
+      hctl->nbig = rehist ? 0u : tb;
+    }
+    if (!rehist && (nt | nb)) {
+      for (int j = 0; j < kHistBins / kSegs; ++j) {
+        const uint32_t bit = 1u << (j & 31);
+        if (tiny_bits[j >> 5] & bit) tiny[ot++] = j * kSegs + s;
+        if (big_bits[j >> 5] & bit) big[ob++] = j * kSegs + s;
+      }
+    }
   }
   if (rehist) {  // shifted window: the bins are sorted as items (see k_local_sort)
     const uint32_t R = (uint32_t)(plan->kb - kTopBits);
@@ -1315,15 +1368,20 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
 template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(kLocalThreads, 2)
     k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
-                 const MsdPlan* __restrict__ msd) {
+                 const MsdPlan* __restrict__ msd, const uint32_t* __restrict__ big, const HeavyCtl* __restrict__ ctl) {
   // (R is the host's key_bits - 16.  A window moved below a common prefix sends
   // every bin to k_heavy_items instead: a loaded R costs ~26 us here at c5 — it
   // takes a register where the kernel parameter is an operand.)
-  const uint32_t bkt = blockIdx.x;
   const uint32_t use = __ldg(&msd->use_msd), rehist = __ldg(&msd->rehist);
+  if (!use) return;
+  uint32_t bkt = blockIdx.x;
+  if (big != nullptr) {  // small inputs: one CTA per listed bin, not one per bin
+    if (bkt >= __ldg(&ctl->nbig)) return;
+    bkt = __ldg(big + bkt);
+  }
   const uint64_t b0 = __ldg(P16 + bkt);
   const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
-  if (!use || m <= 1 || m > (uint32_t)kLocalCap) return;
+  if (m <= kTinyMax || m > (uint32_t)kLocalCap) return;  // tiny bins: k_tiny_bins
 #if FS_LOCAL_REHIST_INLINE
   if (rehist) {  // the window moved below a common prefix: the plan's R and prefix
     const int Rw = __ldg(&msd->kb) - kTopBits;
@@ -1338,6 +1396,54 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 
 #include "wide_heavy.cuh"
 
+// Bins of 2..kTinyMax keys, one warp each (a CTA's barriers and round trips
+// would cost more than the sort): every key's rank = #keys of the bin below it
+// (ties by arrival), by shuffles; in place (all keys are in registers first).
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(256)
+    k_tiny_bins(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16,
+                const uint32_t* __restrict__ list, const HeavyCtl* __restrict__ ctl, const MsdPlan* __restrict__ msd) {
+  constexpr uint32_t kPer = kTinyMax / 32;  // keys per lane
+  if (!msd->use_msd || msd->rehist) return;
+  const uint32_t nt = ctl->ntiny;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nw = gridDim.x * (blockDim.x / 32);
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nw) {
+    const uint32_t v = __ldg(list + t);
+    const uint64_t b0 = __ldg(P16 + v);
+    const uint32_t m = (uint32_t)(__ldg(P16 + v + 1) - b0);  // 2..kTinyMax, warp-uniform
+    K k[kPer];
+    uint32_t val[kPer], r[kPer];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t i = q * 32 + lane;
+      k[q] = i < m ? keys[b0 + i] : K(0);
+      val[q] = (kHasValues && i < m) ? vals[b0 + i] : 0u;
+      r[q] = 0;
+    }
+    for (uint32_t j = 0; j < m; ++j) {
+      K kj = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < kPer; ++q) {
+        const K x = __shfl_sync(kFull, k[q], j & 31u);
+        if ((j >> 5) == q) kj = x;
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < kPer; ++q) r[q] += (kj < k[q]) || (kj == k[q] && j < q * 32 + lane);
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      if (q * 32 + lane < m) {
+        keys[b0 + r[q]] = k[q];
+        if (kHasValues) vals[b0 + r[q]] = val[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
 // ================================================================ driver
 struct WideLayout {
   size_t alt_k = 0, alt_v = 0, partials = 0;
@@ -1345,6 +1451,7 @@ struct WideLayout {
          zero_end = 0;
   size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
   size_t hctl = 0, hseg0 = 0, hseg1 = 0, hsegl2 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // k_heavy
+  size_t htiny = 0, hbig = 0;  // bin lists
   uint64_t tiles = 0, status_tiles = 0;
   uint64_t chunk_tiles = 0;  // MSD: tiles per histogram chunk (= level-1 virtual segment)
   int hgrid = 0;             // MSD: histogram CTAs = chunks
@@ -1363,7 +1470,7 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   // tiles in a segment) fits, level 1 needs chunks x chunk_tiles <= tiles + chunks
   L.status_tiles = L.tiles + (L.use_msd ? L.tiles / 4 + 2 * kSegs : 0);
   const uint64_t sms = (uint64_t)device_info().sm_count;
-  L.chunk_tiles = (L.tiles + sms - 1) / sms;
+  L.chunk_tiles = (L.tiles + sms - 1) / sms;  // (>= 16 tiles per chunk at small n: L1 slower, hist no faster)
   L.hgrid = (int)((L.tiles + L.chunk_tiles - 1) / L.chunk_tiles);
   size_t off = 0;
   L.alt_k = off;
@@ -1414,6 +1521,10 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
     off = align_up(off + sizeof(uint64_t) * kRadix * hc.chunks);
     L.hitems = off;
     off = align_up(off + sizeof(HeavyItem) * hc.items);
+    L.htiny = off;
+    off = align_up(off + sizeof(uint32_t) * kHistBins);
+    L.hbig = off;
+    off = align_up(off + sizeof(uint32_t) * kHistBins);
   }
   L.lsd = off;
   off = align_up(off + sizeof(LsdPlan));
@@ -1493,8 +1604,10 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
     auto* hctl = (HeavyCtl*)(t + L.hctl);
+    const bool list_big = n < kListBigMaxN;  // one CTA per bin is cheaper once most bins are large
     k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0),
-                                   (HeavySeg*)(t + L.hsegl2), (HeavyItem*)(t + L.hitems));
+                                   (HeavySeg*)(t + L.hsegl2), (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
+                                   (uint32_t*)(t + L.hbig), list_big ? 1 : 0);
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1544,7 +1657,13 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     if ((e = cudaFuncSetAttribute(k_local_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lsmem)) != cudaSuccess)
       return e;
-    k_local_sort<K, kHasValues><<<kHistBins, kLocalThreads, lsmem, s>>>(kout, vout, P16, key_bits - kTopBits, msd);
+    // small inputs: at most n / 65 bins need a CTA, listed by the plan
+    const unsigned lgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kTinyMax + 1) + 1)
+                                    : (unsigned)kHistBins;
+    k_local_sort<K, kHasValues><<<lgrid, kLocalThreads, lsmem, s>>>(
+        kout, vout, P16, key_bits - kTopBits, msd, list_big ? (const uint32_t*)(t + L.hbig) : nullptr, hctl);
+    k_tiny_bins<K, kHasValues><<<(unsigned)(8 * sms), 256, 0, s>>>(kout, vout, P16, (const uint32_t*)(t + L.htiny),
+                                                                   hctl, msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_heavy_items<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lsmem)) != cudaSuccess)

@@ -283,6 +283,20 @@ def test_msd_narrow_effective_keys_take_lsd(cuda):
     _check_pairs(cuda, k)
 
 
+@pytest.mark.parametrize("n", [1 << 18, (1 << 18) + 3, 700_001, (1 << 21) + 5])
+@pytest.mark.parametrize("kind", ["uniform", "few", "sorted"])
+def test_msd_small_inputs(cuda, n, kind):
+    """MSD from 2^18 pairs: bins of <= 128 keys sorted by one warp each
+    (k_tiny_bins), the others by k_local_sort from the plan's list; ties among
+    duplicates keep arrival order."""
+    k = datagen.gen_u64(n, seed=n % 1013)
+    if kind == "few":  # ~16 keys per distinct value: tiny bins full of ties
+        k = k[datagen.gen_u64(n, seed=3) % np.uint64(max(1, n // 16))]
+    elif kind == "sorted":
+        k = np.sort(k)
+    _check_pairs(cuda, k)
+
+
 def test_msd_unaligned_buffers(cuda):
     """Inputs/outputs not 16-byte aligned: the scatter passes load tiles without bulk copies."""
     n = (1 << 22) + 5
