@@ -270,7 +270,7 @@ def run_fs_pairs(args, dev):
                        "method_GBps": round(method_b / (t_step * 1e-3) / 1e9, 1),
                        "frac_method_of_measured_peak": round(method_b / (t_step * 1e-3) / 1e9 / peak, 4)},
         "phases_ms": {nm: round(x, 4) for nm, x in zip(names, phase)},
-        "gpu_launches": 21 * steps,  # MSD: 10 kernels (hist, scan, plan, 2 vseg, 2 scatters, local, recursion, items); LSD: 11 (return at once)
+        "gpu_launches": 25 * steps,  # MSD: 14 kernels (2 hist, window x2, scan, plan, 2 vseg, 2 scatters, heavy, local, tiny, items); LSD: 11 (return at once)
         "clocks": clocks.summary(),
     }
     if not args.no_verify:
@@ -413,7 +413,7 @@ def run_fs(args, rank, world, local_rank):
         "phases_ms": {k: round(v, 5) for k, v in zip(
             (["prologue", "hist16+merge+scan", "expand16"] if world == 1 else ["hist16+merge+scan", "nccl_allreduce", "expand16"]),
             phase_ms)},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if (world == 1 and n <= (1 << 18)) else 2) * args.steps,  # one cluster launch up to 2^18
         "clocks": clocks.summary(),
         "phase_events": f"recorded on every {PHASE_EVERY}th of the {args.steps} timed steps ({len(events)} steps); "
                         "ms_per_step from events bracketing the whole timed region",
