@@ -127,7 +127,6 @@ constexpr int kSegs = 256;              // first-level segments
 #define FS_LOCAL_CB 12
 #endif
 constexpr int kLocalThreads = FS_LOCAL_THREADS;
-constexpr int kLocalWarps = kLocalThreads / 32;
 constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in shared memory
 constexpr int kIdxBits = 14;            // local index bits of the composite key
 static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
@@ -142,6 +141,7 @@ constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 #endif
 constexpr uint64_t kMsdMinN = FS_MSD_MIN_N;
 constexpr uint32_t kTinyMax = FS_TINY_MAX;
+constexpr int kMidCap = 2048;  // bins of kTinyMax+1 .. 2,048 keys: k_local_mid (smaller CTAs, 4 per SM)
 constexpr uint64_t kListBigMaxN = 1ull << 26;  // below: k_local_sort runs from the plan's list of bins
   // bins of <= 64 keys: one warp each (k_tiny_bins), not a CTA
 
@@ -198,6 +198,7 @@ struct HeavyCtl {
   uint32_t nitems;
   uint32_t ntiny;                           // bins of 2..kTinyMax keys (k_tiny_bins)
   uint32_t nbig;                            // bins for k_local_sort when it runs from a list (small inputs)
+  uint32_t nmid;                            // bins of kTinyMax+1 .. kMidCap keys (k_local_mid)
 };
 
 struct HeavyCaps {
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(kSegs)
     k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
                MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
                HeavySeg* __restrict__ hl2, HeavyItem* __restrict__ hitems, uint32_t* __restrict__ tiny,
-               uint32_t* __restrict__ big, int list_big) {
+               uint32_t* __restrict__ big, uint32_t* __restrict__ mid, int list_big) {
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
   __shared__ int one_bin;
@@ -597,6 +598,7 @@ __global__ void __launch_bounds__(kSegs)
   __syncthreads();
   uint32_t tiny_bits[kHistBins / kSegs / 32] = {};  // bins of 2..kTinyMax keys (bit j: bin j * 256 + s)
   uint32_t big_bits[kHistBins / kSegs / 32] = {};   // bins for k_local_sort (listed only for small inputs)
+  uint32_t mid_bits[kHistBins / kSegs / 32] = {};   // bins for k_local_mid
 #pragma unroll 16
   for (int j = 0; j < kHistBins / kSegs; ++j) {  // coalesced, 16 loads in flight per thread
     const uint32_t v = j * kSegs + s;
@@ -604,42 +606,47 @@ __global__ void __launch_bounds__(kSegs)
     if (c == n) one_bin = 1;
     if (c > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{P16[v], c, 0, 0, 0, 0};
     if (c >= 2 && c <= kTinyMax) tiny_bits[j >> 5] |= 1u << (j & 31);
-    if (list_big && c > kTinyMax && c <= (uint64_t)kLocalCap) big_bits[j >> 5] |= 1u << (j & 31);
+    if (c > kTinyMax && c <= (uint64_t)kMidCap) mid_bits[j >> 5] |= 1u << (j & 31);
+    if (list_big && c > (uint64_t)kMidCap && c <= (uint64_t)kLocalCap) big_bits[j >> 5] |= 1u << (j & 31);
   }
-  {  // lists of the tiny bins (2..kTinyMax keys) and, for small inputs, of the
-     // others the local sort takes: offsets by a block scan (no atomics)
-    __shared__ uint32_t lsum[2][kSegs / 32];
-    uint32_t nt = 0, nb = 0;
+  {  // lists of the tiny bins (2..kTinyMax keys), the mid bins (..kMidCap) and,
+     // for small inputs, of the others: offsets by a block scan (no atomics)
+    __shared__ uint32_t lsum[3][kSegs / 32];
+    uint32_t c3[3] = {0, 0, 0};
 #pragma unroll
     for (int q = 0; q < kHistBins / kSegs / 32; ++q) {
-      nt += __popc(tiny_bits[q]);
-      nb += __popc(big_bits[q]);
+      c3[0] += __popc(tiny_bits[q]);
+      c3[1] += __popc(mid_bits[q]);
+      c3[2] += __popc(big_bits[q]);
     }
-    const uint32_t it = warp_inclusive_scan<uint32_t>(nt), ib = warp_inclusive_scan<uint32_t>(nb);
-    if (lane == 31) {
-      lsum[0][warp] = it;
-      lsum[1][warp] = ib;
+    uint32_t off[3], tot[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const uint32_t inc = warp_inclusive_scan<uint32_t>(c3[l]);
+      if (lane == 31) lsum[l][warp] = inc;
+      off[l] = inc - c3[l];
     }
     __syncthreads();
-    uint32_t ot = it - nt, ob = ib - nb, tt = 0, tb = 0;
 #pragma unroll
-    for (int w = 0; w < kSegs / 32; ++w) {
-      if (w < (int)warp) {
-        ot += lsum[0][w];
-        ob += lsum[1][w];
+    for (int l = 0; l < 3; ++l) {
+      tot[l] = 0;
+#pragma unroll
+      for (int w = 0; w < kSegs / 32; ++w) {
+        if (w < (int)warp) off[l] += lsum[l][w];
+        tot[l] += lsum[l][w];
       }
-      tt += lsum[0][w];
-      tb += lsum[1][w];
     }
     if (s == 0) {
-      hctl->ntiny = rehist ? 0u : tt;
-      hctl->nbig = rehist ? 0u : tb;
+      hctl->ntiny = rehist ? 0u : tot[0];
+      hctl->nmid = rehist ? 0u : tot[1];
+      hctl->nbig = rehist ? 0u : tot[2];
     }
-    if (!rehist && (nt | nb)) {
+    if (!rehist && (c3[0] | c3[1] | c3[2])) {
       for (int j = 0; j < kHistBins / kSegs; ++j) {
         const uint32_t bit = 1u << (j & 31);
-        if (tiny_bits[j >> 5] & bit) tiny[ot++] = j * kSegs + s;
-        if (big_bits[j >> 5] & bit) big[ob++] = j * kSegs + s;
+        if (tiny_bits[j >> 5] & bit) tiny[off[0]++] = j * kSegs + s;
+        if (mid_bits[j >> 5] & bit) mid[off[1]++] = j * kSegs + s;
+        if (big_bits[j >> 5] & bit) big[off[2]++] = j * kSegs + s;
       }
     }
   }
@@ -1088,18 +1095,32 @@ FS_DEVINL void prefetch_l2_range(const void* b, const void* e) {
   }
 }
 
-struct LocalSmemLayout {
-  static constexpr int ck = 0;                                      // u64[kLocalCap]
-  static constexpr int perm = ck + kLocalCap * 8;                   // u16[kLocalCap]
-  static constexpr int scratch = perm + kLocalCap * 2;
+// Geometry of one per-bin sort: kThreads (>= 256: the slow path's digit scan
+// uses one thread per digit) and the largest bin kCap.
+template <int kThreads_, int kCap_>
+struct LocalCfg {
+  static constexpr int kThreads = kThreads_, kWarps = kThreads_ / 32, kCap = kCap_;
+  static constexpr int kPer = (kCap + kThreads - 1) / kThreads;  // composites per thread
+  static_assert(kThreads >= kRadix, "one thread per digit in the slow path");
+  static_assert(kCap <= (1 << kIdxBits), "local index must fit");
+};
+using BigCfg = LocalCfg<kLocalThreads, kLocalCap>;  // 16-bit bins up to 8,704 keys, 2 CTAs per SM
+using MidCfg = LocalCfg<256, kMidCap>;             // bins of kTinyMax+1 .. kMidCap keys, 4 CTAs per SM
+
+template <class Cfg>
+struct LocalLayout {
+  static constexpr int ck = 0;                                      // u64[kCap]
+  static constexpr int perm = ck + Cfg::kCap * 8;                   // u16[kCap]
+  static constexpr int scratch = perm + Cfg::kCap * 2;
   // fast path: counters u16[2^kCountBitsMax]; the final permutation lives in `perm`
-  // slow path: perm_b u16[kLocalCap], then per-warp digit offsets u16[16][256]
+  // slow path: perm_b u16[kCap], then per-warp digit offsets u16[warps][256]
   static constexpr int perm_b = scratch;
-  static constexpr int whist = scratch + kLocalCap * 2;
+  static constexpr int whist = scratch + Cfg::kCap * 2;
   static constexpr int fast_end = scratch + (1 << kCountBitsMax) * 2;
-  static constexpr int slow_end = whist + kLocalWarps * kRadix * 2;
+  static constexpr int slow_end = whist + Cfg::kWarps * kRadix * 2;
   static constexpr int total = fast_end > slow_end ? fast_end : slow_end;
 };
+using LocalSmemLayout = LocalLayout<BigCfg>;
 static_assert(LocalSmemLayout::total <= 113 * 1024, "two CTAs per SM");
 
 // per-bin sort of Alg. 5 ("sort_bin"), stable: every key of
@@ -1116,9 +1137,12 @@ static_assert(LocalSmemLayout::total <= 113 * 1024, "two CTAs per SM");
 //    8-bit digits of the R bits on the permutation (warp multisplit ranks).
 // Output: kout[b0 + j] = top + (c_j >> 14), vout[b0 + j] = vin[b0 + i_j]; kin == kout
 // (in place) is allowed: every key is in registers before the first store.
-template <typename K, bool kHasValues>
+template <typename K, bool kHasValues, class Cfg = BigCfg>
 __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t b0,
                                          uint32_t m, int R, K top) {
+  using Lay = LocalLayout<Cfg>;
+  constexpr int kLocalThreads = Cfg::kThreads, kLocalWarps = Cfg::kWarps, kLocalCap = Cfg::kCap;
+  (void)kLocalCap;
 #ifdef FS_SCATTER_STATS
   long long lph_t0 = clock64();
 #endif
@@ -1126,9 +1150,9 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   // now (4.38 vs 4.41 ms at c5; prefetching the bin one wave ahead did nothing).
   if (kHasValues && threadIdx.x == 0) prefetch_l2_range(vin + b0, vin + b0 + m);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* ck = reinterpret_cast<uint64_t*>(smem_raw + LocalSmemLayout::ck);
-  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::perm);
-  uint32_t* cntw = reinterpret_cast<uint32_t*>(smem_raw + LocalSmemLayout::scratch);
+  uint64_t* ck = reinterpret_cast<uint64_t*>(smem_raw + Lay::ck);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm);
+  uint32_t* cntw = reinterpret_cast<uint32_t*>(smem_raw + Lay::scratch);
   uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cntw);
   __shared__ uint32_t heavy;
   __shared__ uint32_t wtot[kLocalWarps];
@@ -1147,7 +1171,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   // registers; the digit histogram is counted from them; after the scan each
   // composite is written straight to its group's slot (ck is filled in group
   // order, never in arrival order: the arrival index is in the composite).
-  constexpr int kPer = (kLocalCap + kLocalThreads - 1) / kLocalThreads;  // 17
+  constexpr int kPer = Cfg::kPer;  // 17 (big), 8 (mid)
   uint64_t cr[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
@@ -1249,8 +1273,8 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   if (heavy) {
     // ---- slow path: stable LSD over the varying 8-bit digits of the R bits
     uint16_t* pa = perm;
-    uint16_t* pb = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::perm_b);
-    uint16_t* wh16 = reinterpret_cast<uint16_t*>(smem_raw + LocalSmemLayout::whist);  // [warp][digit]
+    uint16_t* pb = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm_b);
+    uint16_t* wh16 = reinterpret_cast<uint16_t*>(smem_raw + Lay::whist);  // [warp][digit]
     if (tid == 0) {
       or_all = 0;
       and_all = ~0ull;
@@ -1381,7 +1405,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   }
   const uint64_t b0 = __ldg(P16 + bkt);
   const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
-  if (m <= kTinyMax || m > (uint32_t)kLocalCap) return;  // tiny bins: k_tiny_bins
+  if (m <= (uint32_t)kMidCap || m > (uint32_t)kLocalCap) return;  // tiny / mid bins: their own kernels
 #if FS_LOCAL_REHIST_INLINE
   if (rehist) {  // the window moved below a common prefix: the plan's R and prefix
     const int Rw = __ldg(&msd->kb) - kTopBits;
@@ -1392,6 +1416,25 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
   if (rehist) return;
 #endif
   sort_bin<K, kHasValues>(keys, vals, keys, vals, b0, m, R, (K)((uint64_t)bkt << R));
+}
+
+
+// Bins of kTinyMax+1 .. kMidCap keys: the same per-bin sort with 256 threads and
+// a 2,048-key shared layout, so four bins are in flight per SM instead of two.
+// One CTA per listed bin (small inputs) or a persistent loop over the list.
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(MidCfg::kThreads, 4)
+    k_local_mid(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
+                const uint32_t* __restrict__ list, const HeavyCtl* __restrict__ ctl, const MsdPlan* __restrict__ msd) {
+  if (!__ldg(&msd->use_msd) || __ldg(&msd->rehist)) return;
+  const uint32_t nm = __ldg(&ctl->nmid);
+  for (uint32_t i = blockIdx.x; i < nm; i += gridDim.x) {
+    const uint32_t bkt = __ldg(list + i);
+    const uint64_t b0 = __ldg(P16 + bkt);
+    const uint32_t m = (uint32_t)(__ldg(P16 + bkt + 1) - b0);
+    sort_bin<K, kHasValues, MidCfg>(keys, vals, keys, vals, b0, m, R, (K)((uint64_t)bkt << R));
+    __syncthreads();
+  }
 }
 
 #include "wide_heavy.cuh"
@@ -1451,7 +1494,7 @@ struct WideLayout {
          zero_end = 0;
   size_t H16 = 0, P16 = 0, vcnt = 0, vbase = 0, lsd = 0, msd = 0, total = 0;
   size_t hctl = 0, hseg0 = 0, hseg1 = 0, hsegl2 = 0, hchunk = 0, hchist = 0, hcbase = 0, hitems = 0;  // k_heavy
-  size_t htiny = 0, hbig = 0;  // bin lists
+  size_t htiny = 0, hbig = 0, hmid = 0;  // bin lists
   uint64_t tiles = 0, status_tiles = 0;
   uint64_t chunk_tiles = 0;  // MSD: tiles per histogram chunk (= level-1 virtual segment)
   int hgrid = 0;             // MSD: histogram CTAs = chunks
@@ -1524,6 +1567,8 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
     L.htiny = off;
     off = align_up(off + sizeof(uint32_t) * kHistBins);
     L.hbig = off;
+    off = align_up(off + sizeof(uint32_t) * kHistBins);
+    L.hmid = off;
     off = align_up(off + sizeof(uint32_t) * kHistBins);
   }
   L.lsd = off;
@@ -1607,7 +1652,7 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     const bool list_big = n < kListBigMaxN;  // one CTA per bin is cheaper once most bins are large
     k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0),
                                    (HeavySeg*)(t + L.hsegl2), (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
-                                   (uint32_t*)(t + L.hbig), list_big ? 1 : 0);
+                                   (uint32_t*)(t + L.hbig), (uint32_t*)(t + L.hmid), list_big ? 1 : 0);
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1658,12 +1703,20 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
                                   lsmem)) != cudaSuccess)
       return e;
     // small inputs: at most n / 65 bins need a CTA, listed by the plan
-    const unsigned lgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kTinyMax + 1) + 1)
+    const unsigned lgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kMidCap + 1) + 1)
                                     : (unsigned)kHistBins;
     k_local_sort<K, kHasValues><<<lgrid, kLocalThreads, lsmem, s>>>(
         kout, vout, P16, key_bits - kTopBits, msd, list_big ? (const uint32_t*)(t + L.hbig) : nullptr, hctl);
     k_tiny_bins<K, kHasValues><<<(unsigned)(8 * sms), 256, 0, s>>>(kout, vout, P16, (const uint32_t*)(t + L.htiny),
                                                                    hctl, msd);
+    constexpr int msmem = LocalLayout<MidCfg>::total;
+    if ((e = cudaFuncSetAttribute(k_local_mid<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  msmem)) != cudaSuccess)
+      return e;
+    const unsigned mgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kTinyMax + 1) + 1)
+                                    : (unsigned)(4 * sms);  // large inputs: few mid bins, a persistent loop
+    k_local_mid<K, kHasValues><<<mgrid, MidCfg::kThreads, msmem, s>>>(kout, vout, P16, key_bits - kTopBits,
+                                                                      (const uint32_t*)(t + L.hmid), hctl, msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_heavy_items<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lsmem)) != cudaSuccess)
