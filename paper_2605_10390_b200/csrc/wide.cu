@@ -199,6 +199,7 @@ struct HeavyCtl {
   uint32_t ntiny;                           // bins of 2..kTinyMax keys (k_tiny_bins)
   uint32_t nbig;                            // bins for k_local_sort when it runs from a list (small inputs)
   uint32_t nmid;                            // bins of kTinyMax+1 .. kMidCap keys (k_local_mid)
+  uint32_t one_bin;                         // one 16-bit bin holds every key (k_bin_lists)
 };
 
 struct HeavyCaps {
@@ -576,89 +577,96 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// MSD plan: the tiles of the level-2 pass (segments = first-level buckets,
-// bounds from P16), and the first level of the recursion: every 16-bit bin
-// above the local-sort capacity becomes a heavy segment.  If one bin holds all
-// the keys (a common 16-bit prefix: the MSD levels would move everything for
-// nothing) the LSD path runs instead, skipping its uniform digits.
-__global__ void __launch_bounds__(kSegs)
-    k_msd_plan(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n, uint32_t status_cap,
-               MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
-               HeavySeg* __restrict__ hl2, HeavyItem* __restrict__ hitems, uint32_t* __restrict__ tiny,
-               uint32_t* __restrict__ big, uint32_t* __restrict__ mid, int list_big) {
-  __shared__ uint32_t wsum[kSegs / 32];
-  __shared__ uint32_t rmax;
-  __shared__ int one_bin;
-  const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
+// The 16-bit bins, classified (many CTAs; every append is one atomic per CTA):
+// above the local-sort capacity -> the recursion's first segments; 2..kTinyMax
+// keys -> k_tiny_bins; ..kMidCap -> k_local_mid; the rest -> k_local_sort's list
+// (small inputs only; large ones run one CTA per bin).  With a moved window
+// (rehist) every bin of 2..cap keys becomes a k_heavy_items item instead.
+constexpr int kListThreads = 256;
+constexpr int kListBinsPerThread = 4;
+constexpr int kListGrid = kHistBins / (kListThreads * kListBinsPerThread);  // 64
+
+__global__ void __launch_bounds__(kListThreads)
+    k_bin_lists(const uint64_t* __restrict__ H16, const uint64_t* __restrict__ P16, uint64_t n,
+                const MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
+                HeavyItem* __restrict__ hitems, uint32_t* __restrict__ tiny, uint32_t* __restrict__ mid,
+                uint32_t* __restrict__ big, int list_big) {
+  __shared__ uint32_t lsum[4][kListThreads / 32];
+  __shared__ uint32_t lbase[4];
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
   const uint32_t rehist = plan->rehist;
-  if (s == 0) {
-    one_bin = 0;
-    rmax = 0;
+  const uint32_t R = (uint32_t)(plan->kb - kTopBits);
+  uint64_t c[kListBinsPerThread];
+  uint32_t v[kListBinsPerThread];
+#pragma unroll
+  for (int i = 0; i < kListBinsPerThread; ++i) {
+    v[i] = blockIdx.x * (kListThreads * kListBinsPerThread) + i * kListThreads + t;
+    c[i] = __ldg(H16 + v[i]);
+  }
+  uint32_t cls[kListBinsPerThread];  // 0 tiny, 1 mid, 2 big (listed), 3 item (rehist), 4 none
+  uint32_t cnt[4] = {0, 0, 0, 0};
+  bool one = false;
+#pragma unroll
+  for (int i = 0; i < kListBinsPerThread; ++i) {
+    one |= c[i] == n;
+    if (c[i] > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{__ldg(P16 + v[i]), c[i], 0, 0, 0, 0};
+    uint32_t k = 4;
+    if (c[i] >= 2 && c[i] <= (uint64_t)kLocalCap) {
+      if (rehist) k = 3;
+      else if (c[i] <= kTinyMax) k = 0;
+      else if (c[i] <= (uint64_t)kMidCap) k = 1;
+      else if (list_big) k = 2;
+    }
+    cls[i] = k;
+    if (k < 4) ++cnt[k];
+  }
+  if (one) hctl->one_bin = 1u;
+  uint32_t off[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const uint32_t inc = warp_inclusive_scan<uint32_t>(cnt[l]);
+    if (lane == 31) lsum[l][warp] = inc;
+    off[l] = inc - cnt[l];
   }
   __syncthreads();
-  uint32_t tiny_bits[kHistBins / kSegs / 32] = {};  // bins of 2..kTinyMax keys (bit j: bin j * 256 + s)
-  uint32_t big_bits[kHistBins / kSegs / 32] = {};   // bins for k_local_sort (listed only for small inputs)
-  uint32_t mid_bits[kHistBins / kSegs / 32] = {};   // bins for k_local_mid
-#pragma unroll 16
-  for (int j = 0; j < kHistBins / kSegs; ++j) {  // coalesced, 16 loads in flight per thread
-    const uint32_t v = j * kSegs + s;
-    const uint64_t c = __ldg(H16 + v);
-    if (c == n) one_bin = 1;
-    if (c > (uint64_t)kLocalCap) hseg[atomicAdd(&hctl->nseg[0], 1u)] = HeavySeg{P16[v], c, 0, 0, 0, 0};
-    if (c >= 2 && c <= kTinyMax) tiny_bits[j >> 5] |= 1u << (j & 31);
-    if (c > kTinyMax && c <= (uint64_t)kMidCap) mid_bits[j >> 5] |= 1u << (j & 31);
-    if (list_big && c > (uint64_t)kMidCap && c <= (uint64_t)kLocalCap) big_bits[j >> 5] |= 1u << (j & 31);
+  if (t < 4) {  // one atomic per list and CTA
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kListThreads / 32; ++w) tot += lsum[t][w];
+    uint32_t* ctr = t == 0 ? &hctl->ntiny : t == 1 ? &hctl->nmid : t == 2 ? &hctl->nbig : &hctl->nitems;
+    lbase[t] = tot ? atomicAdd(ctr, tot) : 0u;
   }
-  {  // lists of the tiny bins (2..kTinyMax keys), the mid bins (..kMidCap) and,
-     // for small inputs, of the others: offsets by a block scan (no atomics)
-    __shared__ uint32_t lsum[3][kSegs / 32];
-    uint32_t c3[3] = {0, 0, 0};
+  __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kHistBins / kSegs / 32; ++q) {
-      c3[0] += __popc(tiny_bits[q]);
-      c3[1] += __popc(mid_bits[q]);
-      c3[2] += __popc(big_bits[q]);
-    }
-    uint32_t off[3], tot[3];
+  for (int l = 0; l < 4; ++l) {
 #pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const uint32_t inc = warp_inclusive_scan<uint32_t>(c3[l]);
-      if (lane == 31) lsum[l][warp] = inc;
-      off[l] = inc - c3[l];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      tot[l] = 0;
-#pragma unroll
-      for (int w = 0; w < kSegs / 32; ++w) {
-        if (w < (int)warp) off[l] += lsum[l][w];
-        tot[l] += lsum[l][w];
-      }
-    }
-    if (s == 0) {
-      hctl->ntiny = rehist ? 0u : tot[0];
-      hctl->nmid = rehist ? 0u : tot[1];
-      hctl->nbig = rehist ? 0u : tot[2];
-    }
-    if (!rehist && (c3[0] | c3[1] | c3[2])) {
-      for (int j = 0; j < kHistBins / kSegs; ++j) {
-        const uint32_t bit = 1u << (j & 31);
-        if (tiny_bits[j >> 5] & bit) tiny[off[0]++] = j * kSegs + s;
-        if (mid_bits[j >> 5] & bit) mid[off[1]++] = j * kSegs + s;
-        if (big_bits[j >> 5] & bit) big[off[2]++] = j * kSegs + s;
-      }
-    }
+    for (int w = 0; w < kListThreads / 32; ++w)
+      if (w < (int)warp) off[l] += lsum[l][w];
+    off[l] += lbase[l];
   }
-  if (rehist) {  // shifted window: the bins are sorted as items (see k_local_sort)
-    const uint32_t R = (uint32_t)(plan->kb - kTopBits);
-    for (int j = 0; j < kHistBins / kSegs; ++j) {
-      const uint32_t v = j * kSegs + s;
-      const uint64_t c = H16[v];
-      if (!FS_LOCAL_REHIST_INLINE && c > 1 && c <= (uint64_t)kLocalCap)
-        hitems[atomicAdd(&hctl->nitems, 1u)] = HeavyItem{P16[v], c, plan->prefix | ((uint64_t)v << R), R, 0};
-    }
+#pragma unroll
+  for (int i = 0; i < kListBinsPerThread; ++i) {
+    const uint32_t k = cls[i];
+    if (k == 0) tiny[off[0]++] = v[i];
+    else if (k == 1) mid[off[1]++] = v[i];
+    else if (k == 2) big[off[2]++] = v[i];
+    else if (k == 3 && !FS_LOCAL_REHIST_INLINE)
+      hitems[off[3]++] = HeavyItem{__ldg(P16 + v[i]), c[i], plan->prefix | ((uint64_t)v[i] << R), R, 0};
   }
+}
+
+// MSD plan: the tiles of the level-2 pass (segments = first-level buckets,
+// bounds from P16).  If one 16-bit bin holds all the keys (k_bin_lists: a common
+// prefix the window could not move below) the LSD path runs instead, skipping
+// its uniform digits.
+__global__ void __launch_bounds__(kSegs)
+    k_msd_plan(const uint64_t* __restrict__ P16, uint32_t status_cap, MsdPlan* __restrict__ plan,
+               HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hl2) {
+  __shared__ uint32_t wsum[kSegs / 32];
+  __shared__ uint32_t rmax;
+  const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
+  if (s == 0) rmax = 0;
+  __syncthreads();
   // Level 2: interleaved tickets (k_scatter mode 2) keep every bucket's lookback
   // one tile deep, but cost 256 x (most tiles in one bucket) status rows.  A
   // bucket above status_cap / 256 tiles (about 1.25x the mean) is left out of
@@ -692,7 +700,7 @@ __global__ void __launch_bounds__(kSegs)
   }
   __syncthreads();
   if (s == 0) {
-    plan->use_msd = one_bin ? 0u : 1u;
+    plan->use_msd = __ldcg(&hctl->one_bin) ? 0u : 1u;
     plan->l2_rmax = rmax;
     plan->l2_interleave = 1u;
   }
@@ -1650,9 +1658,10 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
       return e;
     auto* hctl = (HeavyCtl*)(t + L.hctl);
     const bool list_big = n < kListBigMaxN;  // one CTA per bin is cheaper once most bins are large
-    k_msd_plan<<<1, kSegs, 0, s>>>(H16, P16, n, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hseg0),
-                                   (HeavySeg*)(t + L.hsegl2), (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
-                                   (uint32_t*)(t + L.hbig), (uint32_t*)(t + L.hmid), list_big ? 1 : 0);
+    k_bin_lists<<<kListGrid, kListThreads, 0, s>>>(H16, P16, n, msd, hctl, (HeavySeg*)(t + L.hseg0),
+                                                   (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
+                                                   (uint32_t*)(t + L.hmid), (uint32_t*)(t + L.hbig), list_big ? 1 : 0);
+    k_msd_plan<<<1, kSegs, 0, s>>>(P16, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hsegl2));
     k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
     k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
