@@ -103,7 +103,7 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
 /* ----------------------------------------------------------------------------
  * fs_sort_keys_u32 / fs_sort_keys_u64 — keys-only ascending sort of wider keys.
  * Two schemes with the same (unique) result:
- *  - trie-binned MSD (NEXT-1; n >= 2^18 and key_bits >= 32): one read builds the
+ *  - trie-binned MSD (NEXT-1; n >= 2^15 and key_bits >= 32): one read builds the
  *    leaf level of a 16-level compressed trie over the top 16 key bits; its
  *    level-8 and level-16 counters bound two stable 8-bit MSD scatters; every
  *    16-bit bin is then sorted by its remaining bits in shared memory (Alg. 5's
@@ -299,7 +299,7 @@ fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out,
  *   fs_sort_keys_u16:  [0] start, [1] after zeroing the temp counters, [2] after
  *                      the histogram+merge+scan kernel, [3] after the expansion
  *                      kernel;
- *   wide sorts, MSD planned (n >= 2^18, key_bits >= 32): [0] start, [1] after
+ *   wide sorts, MSD planned (n >= 2^15, key_bits >= 32): [0] start, [1] after
  *                      the trie histogram + scan + plan, [2] level-1 scatter,
  *                      [3] level-2 scatter, [4] k_heavy: level 2 of uneven
  *                      first-level buckets and the recursion into the bins

@@ -283,10 +283,10 @@ def test_msd_narrow_effective_keys_take_lsd(cuda):
     _check_pairs(cuda, k)
 
 
-@pytest.mark.parametrize("n", [1 << 18, (1 << 18) + 3, 700_001, (1 << 21) + 5])
+@pytest.mark.parametrize("n", [(1 << 15) - 1, 1 << 15, 50_001, 1 << 18, 700_001, (1 << 21) + 5])
 @pytest.mark.parametrize("kind", ["uniform", "few", "sorted"])
 def test_msd_small_inputs(cuda, n, kind):
-    """MSD from 2^18 pairs: bins of <= 128 keys sorted by one warp each
+    """MSD from 2^15 pairs: bins of <= 128 keys sorted by one warp each
     (k_tiny_bins), the others by k_local_sort from the plan's list; ties among
     duplicates keep arrival order."""
     k = datagen.gen_u64(n, seed=n % 1013)
