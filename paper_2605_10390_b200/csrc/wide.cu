@@ -1445,6 +1445,124 @@ __global__ void __launch_bounds__(MidCfg::kThreads, 4)
   }
 }
 
+
+// ---- small inputs (n <= kSmallSortMax): the whole sort in one CTA's shared
+// memory — keys and values staged once, a stable LSD over the digits that vary
+// on a u16 permutation (warp multisplit ranks, as sort_bin's slow path), the
+// output written through the permutation.  Eleven launches of the LSD path cost ~80 us of launch
+// latency at 1,000 pairs.
+constexpr int kSmallSortMax = 8192;
+constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+template <typename K, bool kHasValues>
+struct SmallSmem {
+  K keys[kSmallSortMax];
+  uint32_t vals[kHasValues ? kSmallSortMax : 1];
+  uint16_t pa[kSmallSortMax], pb[kSmallSortMax];
+  uint16_t wh[kSmallWarps][kRadix];
+  uint32_t wtot[kSmallWarps];
+  unsigned long long or_all, nor_all;
+};
+
+template <typename K, bool kHasValues>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_small_sort(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+                 uint32_t* __restrict__ vout, uint32_t n, int key_bits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SmallSmem<K, kHasValues>*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    sm.or_all = 0;
+    sm.nor_all = 0;
+  }
+  __syncthreads();
+  unsigned long long o = 0, no = 0;
+  for (uint32_t i = tid; i < n; i += kSmallThreads) {
+    const K k = kin[i];
+    sm.keys[i] = k;
+    if (kHasValues) sm.vals[i] = vin[i];
+    sm.pa[i] = (uint16_t)i;
+    o |= k;
+    no |= (K)~k;
+  }
+  o = ((unsigned long long)__reduce_or_sync(kFull, (uint32_t)(o >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)o);
+  no = ((unsigned long long)__reduce_or_sync(kFull, (uint32_t)(no >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)no);
+  if (lane == 0) {
+    atomicOr(&sm.or_all, o);
+    atomicOr(&sm.nor_all, no);
+  }
+  __syncthreads();
+  const unsigned long long mask = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1);
+  const unsigned long long varying = sm.or_all & sm.nor_all & mask;
+  uint16_t* pa = sm.pa;
+  uint16_t* pb = sm.pb;
+  const uint32_t chunk = ((n + kSmallWarps - 1) / kSmallWarps + 31) & ~31u;
+  const uint32_t c0 = min(warp * chunk, n), c1 = min(c0 + chunk, n);
+  for (int sh = 0; sh < key_bits; sh += kRadixBits) {
+    if (((varying >> sh) & 0xFFu) == 0) continue;  // every key has this digit: the pass is the identity
+    for (int i = tid; i < kSmallWarps * kRadix; i += kSmallThreads) (&sm.wh[0][0])[i] = 0;
+    __syncthreads();
+    uint16_t* whw = sm.wh[warp];
+    // pass A: per-warp digit counts over the warp's chunk of the current order
+    for (uint32_t j0 = c0; j0 < c1; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool valid = j < c1;
+      const uint32_t dg = valid ? (uint32_t)(sm.keys[pa[j]] >> sh) & 0xFFu : 0u;
+      const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
+      if (valid && lane == 31 - __clz(peers)) whw[dg] = (uint16_t)(whw[dg] + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    // offsets: digit-major, warp-minor (thread d < 256 owns digit d)
+    if (tid < kRadix) {
+      uint32_t tot = 0;
+      for (int w = 0; w < kSmallWarps; ++w) tot += sm.wh[w][tid];
+      const uint32_t inc = warp_inclusive_scan<uint32_t>(tot);
+      if (lane == 31) sm.wtot[warp] = inc;
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+      uint32_t tot = 0;
+      for (int w = 0; w < kSmallWarps; ++w) tot += sm.wh[w][tid];
+      uint32_t run = warp_inclusive_scan<uint32_t>(tot) - tot;
+      for (int w = 0; w < (int)warp; ++w) run += sm.wtot[w];
+      for (int w = 0; w < kSmallWarps; ++w) {
+        const uint32_t c = sm.wh[w][tid];
+        sm.wh[w][tid] = (uint16_t)run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    // pass B: stable ranks, scatter of the permutation
+    for (uint32_t j0 = c0; j0 < c1; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool valid = j < c1;
+      const uint16_t p = valid ? pa[j] : (uint16_t)0;
+      const uint32_t dg = valid ? (uint32_t)(sm.keys[p] >> sh) & 0xFFu : 0u;
+      const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
+      const uint32_t leader = 31 - __clz(peers);
+      uint32_t old = 0;
+      if (valid && lane == leader) {
+        old = whw[dg];
+        whw[dg] = (uint16_t)(old + __popc(peers));
+      }
+      old = __shfl_sync(kFull, old, leader);
+      if (valid) pb[old + __popc(peers & lanemask_lt())] = p;
+      __syncwarp();
+    }
+    __syncthreads();
+    uint16_t* t = pa;
+    pa = pb;
+    pb = t;
+  }
+  for (uint32_t j = tid; j < n; j += kSmallThreads) {
+    const uint32_t p = pa[j];
+    kout[j] = sm.keys[p];
+    if (kHasValues) vout[j] = sm.vals[p];  // staged: in place is safe
+  }
+}
+
 #include "wide_heavy.cuh"
 
 // Bins of 2..kTinyMax keys, one warp each (a CTA's barriers and round trips
@@ -1590,6 +1708,16 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
 template <typename K, bool kHasValues>
 cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int key_bits, void* temp,
                 cudaStream_t s) {
+  if (n <= (uint64_t)kSmallSortMax) {  // one CTA, every pass in shared memory
+    constexpr int smem = (int)sizeof(SmallSmem<K, kHasValues>);
+    cudaError_t e = cudaFuncSetAttribute(k_small_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    phase_event(0, s);
+    k_small_sort<K, kHasValues><<<1, kSmallThreads, smem, s>>>(
+        kin, vin, kout, vout, (uint32_t)n, key_bits <= 0 || key_bits > (int)(8 * sizeof(K)) ? (int)(8 * sizeof(K)) : key_bits);
+    phase_event(1, s);
+    return cudaGetLastError();
+  }
   const WideLayout L = layout(n, sizeof(K), key_bits, kHasValues);
   const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
   char* t = (char*)temp;

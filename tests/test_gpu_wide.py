@@ -297,6 +297,27 @@ def test_msd_small_inputs(cuda, n, kind):
     _check_pairs(cuda, k)
 
 
+@pytest.mark.parametrize("n", [1, 2, 777, 8191, 8192, 8193])
+@pytest.mark.parametrize("key_bits", [13, 32, 64])
+def test_small_single_cta_sort(cuda, n, key_bits):
+    """n <= 8,192: the whole LSD in one CTA's shared memory (k_small_sort), incl.
+    digits skipped because every key shares them; 8,193 takes the multi-kernel path."""
+    k = datagen.gen_u64(n, seed=n + key_bits, key_bits=key_bits)
+    _check_pairs(cuda, k, key_bits)
+    if key_bits <= 32:
+        k32 = k.astype(np.uint32)
+        np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k32, cuda), key_bits=key_bits)),
+                                      oracle.sort_keys_u32(k32, key_bits))
+
+
+def test_small_single_cta_sort_equal_and_few(cuda):
+    """All keys equal (no pass runs: output = input order) and few distinct keys."""
+    k = np.full(5000, 0xDEADBEEF, dtype=np.uint64)
+    _check_pairs(cuda, k)
+    k = datagen.gen_u64(3, seed=4)[datagen.gen_u64(6000, seed=5) % np.uint64(3)]
+    _check_pairs(cuda, k)
+
+
 def test_msd_unaligned_buffers(cuda):
     """Inputs/outputs not 16-byte aligned: the scatter passes load tiles without bulk copies."""
     n = (1 << 22) + 5
