@@ -92,6 +92,9 @@ size_t fs_exclusive_scan_u64_temp_bytes(uint64_t nbins);
  *      PAPER.md:168-190);
  *   3. reconstruction = count-expansion: out[P[v] .. P[v+1]) = v (Alg. 5,
  *      PAPER.md:256-286, with t = 0 and l_b = 0).
+ * n <= 2^18: the three stages run in one launch of a 16-CTA thread-block
+ * cluster (per-CTA histograms merged through L2, the expansion staged in
+ * shared memory); larger n: a cooperative histogram kernel and the expansion.
  * keys_in, keys_out: device arrays of n u16.  keys_out == keys_in (in place) is
  * allowed; any other overlap is FS_ERR_INVALID_ARGUMENT.  key_bits: 0 or 1..16.
  * temp: >= fs_sort_keys_u16_temp_bytes(n) device bytes (contents undefined on
@@ -118,7 +121,8 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
  *    phases", §II) with 8-bit digits and one compressed histogram
  *    per digit, all digit histograms in one read pass (config c5's "multi-digit
  *    precision scaling with compressed histograms per digit", ledger 25); a
- *    digit whose histogram has one non-empty bin is skipped.
+ *    digit whose histogram has one non-empty bin is skipped.  n <= 8,192: the
+ *    same LSD inside one CTA's shared memory (one launch).
  * keys_in and keys_out must not overlap.  key_bits: 0 or 1..32 (u32), 0 or
  * 1..64 (u64).
  * ------------------------------------------------------------------------- */
