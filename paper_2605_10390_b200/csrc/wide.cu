@@ -18,24 +18,29 @@
 //       b. k_scatter mode 1: stable scatter by bits [kb-8, kb) into the
 //          temporary buffer; mode 2: stable scatter by bits [kb-16, kb-8)
 //          within each of the 256 first-level segments, into the output.
-//       c. k_local_sort: every 16-bit bin (<= kLocalCap keys) is sorted in
-//          shared memory by its remaining kb-16 bits, stably, in place.
+//       c. every 16-bit bin is sorted in shared memory by its remaining kb-16
+//          bits, stably, in place: k_local_sort (512 threads, <= kLocalCap
+//          keys), k_local_mid (256 threads, <= kMidCap keys, four per SM),
+//          k_tiny_bins (one warp per bin of <= kTinyMax keys); k_bin_lists
+//          builds their lists.
 //       d. k_heavy (wide_heavy.cuh): bins above kLocalCap recurse on the next
 //          8-bit digits until every piece fits; k_heavy_items sorts the pieces.
-//          k_heavy also runs level 2 when the first-level buckets are too
-//          uneven for the interleaved lookback of (b).
+//          k_heavy also runs level 2 for first-level buckets too large for the
+//          interleaved lookback of (b).
+//       e. a common key prefix moves the 16 bits' window below it
+//          (k_binbits / k_keybits, then k_top16_hist again).
 //     Traffic: 8 (u64 key read) + 3 x 24 = 80 B/pair for c5 (vs 200 for LSD-8);
 //     each recursion level adds 8 + 24 B per pair of the oversize bins.
-// (2) Stable LSD with 8-bit digits (small n / narrow keys, and a common 16-bit
-//     prefix): one read builds all digit histograms (k_digit_hist),
-//     k_digit_plan scans them and skips single-bin digits, then one k_scatter
-//     (mode 0) per digit.
+// (2) Stable LSD with 8-bit digits (small n, fewer than 32 varying key bits):
+//     one read builds all digit histograms (k_digit_hist), k_digit_plan scans
+//     them and skips single-bin digits, then one k_scatter (mode 0) per digit;
+//     n <= kSmallSortMax: the same LSD in one CTA's shared memory (k_small_sort).
 //
-// Choice: the MSD path is taken unless one 16-bit bin holds every key (then the
-// MSD levels would move everything for nothing and LSD skips the uniform
-// digits); keys sharing a prefix first move the MSD window below it
-// (k_binbits / k_keybits) — decided on the device, so nothing synchronises with
-// the host; the kernels of the path not taken return at once.
+// Choice: the host picks by n and key_bits; then the MSD path is taken unless
+// one 16-bit bin holds every key after the window moved (then the MSD levels
+// would move everything for nothing and LSD skips the uniform digits) —
+// decided on the device, so nothing synchronises with the host; the kernels of
+// the path not taken return at once.
 //
 // k_scatter (the "histogram, prefix sum and stable scatter phases"):
 // persistent CTAs (2 per SM for pairs) take 4,096-key tiles in order from an
