@@ -388,3 +388,32 @@ def test_msd_level2_linear_order(cuda):
     ek, ev = oracle.sort_pairs_u64_u32(k, v)
     np.testing.assert_array_equal(to_host(ko), ek)
     np.testing.assert_array_equal(to_host(vo), ev)
+
+
+def test_concurrent_streams(cuda):
+    """Sorts on two CUDA streams at once (one-cluster u16, two-kernel u16, MSD
+    pairs with an oversize bin, u32 keys): the library keeps no state between
+    calls, so concurrent calls with their own temporaries do not interfere."""
+    a16 = datagen.gen_u16("zipf", 200_003, seed=1)
+    b16 = datagen.gen_u16("uniform", (1 << 22) + 1, seed=2)
+    k = datagen.gen_u64((1 << 21) + 3, seed=3)
+    k[:20_000] = (k[:20_000] & np.uint64((1 << 48) - 1)) | np.uint64(0x3333 << 48)
+    v = datagen.iota_u32(k.size)
+    k32 = datagen.gen_u32(3_000_001, seed=4)
+    da, db, dk, dv, d32 = (to_dev(x, cuda) for x in (a16, b16, k, v, k32))
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(device=cuda), torch.cuda.Stream(device=cuda)
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            ra = fs.sort_keys(da)
+            rk, rv = fs.sort_pairs(dk, dv)
+        with torch.cuda.stream(s2):
+            rb = fs.sort_keys(db)
+            r32 = fs.sort_keys(d32)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(to_host(ra), oracle.sort_u16(a16))
+    np.testing.assert_array_equal(to_host(rb), oracle.sort_u16(b16))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(rk), ek)
+    np.testing.assert_array_equal(to_host(rv), ev)
+    np.testing.assert_array_equal(to_host(r32), oracle.sort_keys_u32(k32))
