@@ -417,3 +417,42 @@ def test_concurrent_streams(cuda):
     np.testing.assert_array_equal(to_host(rk), ek)
     np.testing.assert_array_equal(to_host(rv), ev)
     np.testing.assert_array_equal(to_host(r32), oracle.sort_keys_u32(k32))
+
+
+def _fuzz_shape(rng, n):
+    """A random mixture: uniform keys, a common prefix, hot 16-bit bins, few
+    distinct values, sorted runs — so sizes and shapes cross every path (one-CTA
+    LSD, LSD-8, MSD with tiny / mid / large bins, recursion, moved window)."""
+    kb = int(rng.choice([24, 32, 40, 48, 56, 64]))
+    k = datagen.gen_u64(n, seed=int(rng.integers(1 << 30)), key_bits=kb)
+    shape = int(rng.integers(6))
+    if shape == 1 and kb > 20:  # common prefix above a random bit
+        free = int(rng.integers(8, kb))
+        k = (k & np.uint64((1 << free) - 1)) | np.uint64(int(rng.integers(1, 1 << (kb - free))) << free
+                                                       if kb - free < 63 else 0)
+    elif shape == 2:  # hot bins
+        sel = datagen.gen_u64(n, seed=int(rng.integers(1 << 30))) % np.uint64(3) == 0
+        hot = datagen.gen_u64(int(rng.integers(1, 20)), seed=int(rng.integers(1 << 30)), key_bits=kb)
+        k[sel] = hot[datagen.gen_u64(int(sel.sum()), seed=7) % np.uint64(hot.size)] ^ (k[sel] & np.uint64(0xFFF))
+    elif shape == 3:  # few distinct values
+        vals = datagen.gen_u64(int(rng.integers(1, 50)), seed=int(rng.integers(1 << 30)), key_bits=kb)
+        k = vals[k % np.uint64(vals.size)]
+    elif shape == 4:  # sorted runs with noise
+        k = np.sort(k)
+        k[::97] = datagen.gen_u64(k[::97].size, seed=9, key_bits=kb)
+    if kb < 64:
+        k &= np.uint64((1 << kb) - 1)
+    return k, kb
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_fuzz_every_path(cuda, case):
+    rng = np.random.default_rng(5000 + case)
+    lo = 0 if case % 2 else np.log(20_000)  # every other case at least 20,000 keys
+    n = int(np.exp(rng.uniform(lo, np.log(6_000_000))))
+    k, kb = _fuzz_shape(rng, n)
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda), key_bits=kb)
+    ek, ev = oracle.sort_pairs_u64_u32(k, v, kb)
+    np.testing.assert_array_equal(to_host(ko), ek, err_msg=f"n={n} kb={kb}")
+    np.testing.assert_array_equal(to_host(vo), ev, err_msg=f"n={n} kb={kb}")
