@@ -121,7 +121,7 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
  *    phases", §II) with 8-bit digits and one compressed histogram
  *    per digit, all digit histograms in one read pass (config c5's "multi-digit
  *    precision scaling with compressed histograms per digit", ledger 25); a
- *    digit whose histogram has one non-empty bin is skipped.  n <= 8,192: the
+ *    digit whose histogram has one non-empty bin is skipped.  n <= 16,384: the
  *    same LSD inside one CTA's shared memory (one launch).
  * keys_in and keys_out must not overlap.  key_bits: 0 or 1..32 (u32), 0 or
  * 1..64 (u64).

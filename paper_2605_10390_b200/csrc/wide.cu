@@ -1478,18 +1478,17 @@ __global__ void __launch_bounds__(MidCfg::kThreads, 4)
 
 
 // ---- small inputs (n <= kSmallSortMax): the whole sort in one CTA's shared
-// memory — keys and values staged once, a stable LSD over the digits that vary
-// on a u16 permutation (warp multisplit ranks, as sort_bin's slow path), the
-// output written through the permutation.  Eleven launches of the LSD path cost ~80 us of launch
+// memory — the keys staged once, a stable LSD over the digits that vary on a
+// u16 permutation (warp multisplit ranks, as sort_bin's slow path), keys and
+// values written through the permutation (values gathered from the input).  Eleven launches of the LSD path cost ~80 us of launch
 // latency at 1,000 pairs.
-constexpr int kSmallSortMax = 8192;
+constexpr int kSmallSortMax = 16384;  // u64 keys: 128 KB + two u16 permutations 64 KB
 constexpr int kSmallThreads = 512;
 constexpr int kSmallWarps = kSmallThreads / 32;
 
 template <typename K, bool kHasValues>
 struct SmallSmem {
   K keys[kSmallSortMax];
-  uint32_t vals[kHasValues ? kSmallSortMax : 1];
   uint16_t pa[kSmallSortMax], pb[kSmallSortMax];
   uint16_t wh[kSmallWarps][kRadix];
   uint32_t wtot[kSmallWarps];
@@ -1512,7 +1511,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   for (uint32_t i = tid; i < n; i += kSmallThreads) {
     const K k = kin[i];
     sm.keys[i] = k;
-    if (kHasValues) sm.vals[i] = vin[i];
     sm.pa[i] = (uint16_t)i;
     o |= k;
     no |= (K)~k;
@@ -1590,7 +1588,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   for (uint32_t j = tid; j < n; j += kSmallThreads) {
     const uint32_t p = pa[j];
     kout[j] = sm.keys[p];
-    if (kHasValues) vout[j] = sm.vals[p];  // staged: in place is safe
+    if (kHasValues) vout[j] = vin[p];  // inputs and outputs never overlap (ABI)
   }
 }
 

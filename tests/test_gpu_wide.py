@@ -297,11 +297,11 @@ def test_msd_small_inputs(cuda, n, kind):
     _check_pairs(cuda, k)
 
 
-@pytest.mark.parametrize("n", [1, 2, 777, 8191, 8192, 8193])
+@pytest.mark.parametrize("n", [1, 2, 777, 8192, 16383, 16384, 16385])
 @pytest.mark.parametrize("key_bits", [13, 32, 64])
 def test_small_single_cta_sort(cuda, n, key_bits):
-    """n <= 8,192: the whole LSD in one CTA's shared memory (k_small_sort), incl.
-    digits skipped because every key shares them; 8,193 takes the multi-kernel path."""
+    """n <= 16,384: the whole LSD in one CTA's shared memory (k_small_sort), incl.
+    digits skipped because every key shares them; 16,385 takes the multi-kernel path."""
     k = datagen.gen_u64(n, seed=n + key_bits, key_bits=key_bits)
     _check_pairs(cuda, k, key_bits)
     if key_bits <= 32:
