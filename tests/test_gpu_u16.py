@@ -231,3 +231,31 @@ def test_send_counts_matches_oracle(cuda):
             got = to_host(fs.send_counts(Hd, g)).astype(np.uint64)
             np.testing.assert_array_equal(got, oracle.send_counts(hist_all, g))
     del rng
+
+
+def test_c4_full_size_one_gpu(cuda):
+    """Config c4 at full size on one GPU (2^34 keys, 32 GB; bench.py's N = 1
+    launch configuration): the oracle histogram of the input, streamed to the
+    host in chunks, fixes every value's output range; each value's first and
+    last position, 2^20 random positions and the non-decreasing order (checked
+    on the device, chunked) must agree — together they pin the sorted multiset."""
+    n = 1 << 34
+    chunk = 1 << 28
+    keys = torch.empty(n, dtype=torch.uint16, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    datagen.gen_u16_device(keys.data_ptr(), "uniform", n, seed=0, n_total=n, stream=s)
+    out = fs.sort_keys(keys)
+    C = np.zeros(65536, dtype=np.uint64)
+    for a in range(0, n, chunk):
+        C += oracle.histogram_u16(to_host(keys[a:a + chunk]))
+    del keys
+    P = oracle.exclusive_scan(C)
+    nonempty = np.nonzero(C)[0]
+    pos = np.concatenate([P[nonempty], P[nonempty + 1] - 1,
+                          np.random.default_rng(0).integers(0, n, 1 << 20).astype(np.uint64)])
+    want = (np.searchsorted(P, pos, side="right") - 1).astype(np.int64)
+    got = out.view(torch.int16)[torch.from_numpy(pos.astype(np.int64)).to(cuda)].to(torch.int64).cpu().numpy() & 0xFFFF
+    np.testing.assert_array_equal(got, want)
+    for a in range(0, n - 1, chunk):
+        seg = out[a:min(a + chunk + 1, n)].view(torch.int16).to(torch.int32) & 0xFFFF
+        assert bool((seg[1:] >= seg[:-1]).all().item()), f"order broken in [{a}, {a + chunk}]"
