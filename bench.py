@@ -270,7 +270,9 @@ def run_fs_pairs(args, dev):
                        "method_GBps": round(method_b / (t_step * 1e-3) / 1e9, 1),
                        "frac_method_of_measured_peak": round(method_b / (t_step * 1e-3) / 1e9 / peak, 4)},
         "phases_ms": {nm: round(x, 4) for nm, x in zip(names, phase)},
-        "gpu_launches": 25 * steps,  # MSD: 14 kernels (2 hist, window x2, scan, plan, 2 vseg, 2 scatters, heavy, local, tiny, items); LSD: 11 (return at once)
+        # MSD: 16 kernels (2 hist, window x2, scan, lists, plan, 2 vseg, 2 scatters, heavy,
+        # local, tiny, mid, items); LSD: 11 (return at once) -- see profiles/*/launches_c5.csv
+        "gpu_launches": 27 * steps,
         "clocks": clocks.summary(),
     }
     if not args.no_verify:
