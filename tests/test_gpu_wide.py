@@ -456,3 +456,88 @@ def test_fuzz_every_path(cuda, case):
     ek, ev = oracle.sort_pairs_u64_u32(k, v, kb)
     np.testing.assert_array_equal(to_host(ko), ek, err_msg=f"n={n} kb={kb}")
     np.testing.assert_array_equal(to_host(vo), ev, err_msg=f"n={n} kb={kb}")
+
+
+# ---------------------------------------------------------------- maximum sizes
+# Inputs far above c5, checked on the device (a host copy of 24-32 GB would take
+# minutes) by the invariants that pin the unique result: output sorted; values a
+# permutation of 0..n-1 with keys[values] == sorted keys and increasing within
+# equal keys (pairs); per-top-16-bit counts and the key sum preserved (keys).
+# At 2^31 pairs every 16-bit bin (~32,768 pairs) exceeds the local-sort
+# capacity, so the whole input goes through the recursion (k_heavy).
+_SIGN = torch.iinfo(torch.int64).min
+_CHUNK = 1 << 28
+
+
+def _sorted_chunked(x64):
+    prev = None
+    for c0 in range(0, x64.numel(), _CHUNK):
+        b = x64[c0:c0 + _CHUNK]
+        if not bool((b[1:] >= b[:-1]).all().item()) or (prev is not None and not bool((b[0] >= prev).item())):
+            return False
+        prev = b[-1]
+    return True
+
+
+def _free():
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def test_max_size_pairs_2_31(cuda):
+    _free()
+    n = 1 << 31
+    s = torch.cuda.current_stream().cuda_stream
+    k = torch.empty(n, dtype=torch.uint64, device=cuda)
+    v = torch.empty(n, dtype=torch.uint32, device=cuda)
+    datagen.gen_u64_device(k.data_ptr(), n, seed=3, stream=s)
+    datagen.iota_u32_device(v.data_ptr(), n, stream=s)
+    ko, vo = fs.sort_pairs(k, v)
+    del v
+    ko64 = ko.view(torch.int64)
+    assert _sorted_chunked(ko64 ^ _SIGN)
+    idx = vo.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    del vo
+    mark = torch.zeros(n, dtype=torch.uint8, device=cuda)
+    mark[idx] = 1
+    assert bool(mark.all().item())
+    del mark
+    assert bool((k.view(torch.int64)[idx] == ko64).all().item())
+    same = ko64[1:] == ko64[:-1]
+    assert bool((~same | (idx[1:] > idx[:-1])).all().item())
+    del k, ko, ko64, idx, same
+    _free()
+
+
+@pytest.mark.parametrize("dt", [torch.uint32, torch.uint64])
+def test_max_size_keys_2_32(cuda, dt):
+    """n = 2^32 keys: element counts past 32 bits everywhere on the path."""
+    _free()
+    n = 1 << 32
+    s = torch.cuda.current_stream().cuda_stream
+    k = torch.empty(n, dtype=dt, device=cuda)
+    (datagen.gen_u32_device if dt == torch.uint32 else datagen.gen_u64_device)(k.data_ptr(), n, seed=5, stream=s)
+    out = fs.sort_keys(k)
+    hk = torch.zeros(65536, dtype=torch.int64, device=cuda)
+    ho = torch.zeros_like(hk)
+    sk = so = 0
+    prev = None
+    for c0 in range(0, n, _CHUNK):
+        if dt == torch.uint32:
+            a = k[c0:c0 + _CHUNK].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            b = out[c0:c0 + _CHUNK].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            sh = 16
+        else:
+            a = k[c0:c0 + _CHUNK].view(torch.int64) ^ _SIGN
+            b = out[c0:c0 + _CHUNK].view(torch.int64) ^ _SIGN
+            sh = 48
+        assert bool((b[1:] >= b[:-1]).all().item())
+        assert prev is None or bool((b[0] >= prev).item())
+        prev = b[-1]
+        hk += torch.bincount((a >> sh) & 0xFFFF, minlength=65536)
+        ho += torch.bincount((b >> sh) & 0xFFFF, minlength=65536)
+        sk += int((a & 0xFFFFFFF).sum().item())
+        so += int((b & 0xFFFFFFF).sum().item())
+    assert bool((hk == ho).all().item()) and sk == so
+    del k, out, a, b
+    _free()
