@@ -12,7 +12,7 @@ s = torch.cuda.current_stream().cuda_stream
 k = torch.empty(n, dtype=torch.uint64, device=dev); v = torch.empty(n, dtype=torch.uint32, device=dev)
 datagen.gen_u64_device(k.data_ptr(), n, seed=0, stream=s); datagen.iota_u32_device(v.data_ptr(), n, stream=s)
 ko, vo = torch.empty_like(k), torch.empty_like(v)
-names = ["hist", "L1", "L2", "local", "heavy", "lsd"]
+names = ["hist", "L1", "L2", "heavy", "local", "lsd"]
 for path in sorted(glob.glob(os.path.join(ROOT, "scripts/microbench/variants/*.so"))):
     L = ctypes.CDLL(path)
     L.fs_sort_pairs_u64_u32_temp_bytes.restype = ctypes.c_size_t
