@@ -92,6 +92,21 @@ __device__ unsigned long long g_local_phase[8];       // local sort phases (thre
 namespace fs {
 namespace {
 
+#ifndef FS_WIDE_PDL
+#define FS_WIDE_PDL 1
+#endif
+// Programmatic dependent launch between the path's kernels: a kernel launched
+// with launch() may have its CTAs made resident while its predecessor drains,
+// so every such kernel first waits for the predecessor grid (and its memory)
+// to complete; kernels whose CTAs all fit in one wave then let their own
+// successor be launched at once (trigger), the rest at exit.
+FS_DEVINL void pdl_entry(bool trigger) {
+#if FS_WIDE_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
@@ -283,6 +298,7 @@ template <typename K>
 __global__ void __launch_bounds__(512)
     k_digit_hist(const K* __restrict__ keys, uint64_t n, int passes, unsigned long long* __restrict__ hist,
                  const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!lsd_enabled(msd)) return;
   __shared__ uint32_t sh[kMaxPasses * kRadix];
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) sh[i] = 0;
@@ -301,6 +317,7 @@ __global__ void __launch_bounds__(512)
 __global__ void __launch_bounds__(kRadix)
     k_digit_plan(const unsigned long long* __restrict__ hist, uint64_t n, int passes, LsdPlan* __restrict__ plan,
                  const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!lsd_enabled(msd)) return;
   __shared__ uint32_t skip_sh[kMaxPasses];
   __shared__ unsigned long long wsum[kRadix / 32];
@@ -374,6 +391,7 @@ __global__ void __launch_bounds__(1024, 1)
     k_top16_hist(const K* __restrict__ keys, uint64_t n, int shift, uint64_t chunk, uint32_t* __restrict__ partials,
                  unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill,
                  unsigned long long* __restrict__ binbits, const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   constexpr int kPerVec = 16 / sizeof(K);
   constexpr int kUnroll = 4;
   if (msd != nullptr) {
@@ -477,6 +495,7 @@ __global__ void __launch_bounds__(kBinbitsThreads)
     k_binbits(const uint32_t* __restrict__ partials, int rows, unsigned long long* __restrict__ bits,
               uint32_t* __restrict__ done, int key_bits, MsdPlan* __restrict__ msd,
               unsigned long long* __restrict__ spill, uint32_t* __restrict__ l1spill, uint32_t l1spill_words) {
+  pdl_entry(true);
   const uint32_t w = blockIdx.x * kBinbitsThreads + threadIdx.x;  // counter word = bins 2w, 2w + 1
   uint32_t x = 0;
 #pragma unroll 8
@@ -509,6 +528,7 @@ __global__ void __launch_bounds__(1024)
     k_keybits(const K* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ bits, uint32_t* __restrict__ done,
               int key_bits, MsdPlan* __restrict__ msd, unsigned long long* __restrict__ spill,
               uint32_t* __restrict__ l1spill, uint32_t l1spill_words) {
+  pdl_entry(true);
   if (!msd->need_keybits) return;
   unsigned long long o = 0, no = 0;
   constexpr int kPerVec = 16 / sizeof(K);
@@ -562,6 +582,7 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(256)
     k_vseg_counts(const uint32_t* __restrict__ partials, const uint32_t* __restrict__ l1spill,
                   uint32_t* __restrict__ cnt, const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!msd->use_msd) return;
   const uint32_t v = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint4* row = reinterpret_cast<const uint4*>(partials + (uint64_t)v * kHistWords);
@@ -580,6 +601,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_vseg_scan(const uint32_t* __restrict__ cnt, int nseg, const uint64_t* __restrict__ P16,
                 uint64_t* __restrict__ vbase, const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!msd->use_msd) return;
   const uint32_t d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
   uint64_t run = P16[d << 8];
@@ -606,6 +628,7 @@ __global__ void __launch_bounds__(kListThreads)
                 const MsdPlan* __restrict__ plan, HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hseg,
                 HeavyItem* __restrict__ hitems, uint32_t* __restrict__ tiny, uint32_t* __restrict__ mid,
                 uint32_t* __restrict__ big, int list_big) {
+  pdl_entry(true);
   __shared__ uint32_t lsum[4][kListThreads / 32];
   __shared__ uint32_t lbase[4];
   const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
@@ -677,6 +700,7 @@ __global__ void __launch_bounds__(kListThreads)
 __global__ void __launch_bounds__(kSegs)
     k_msd_plan(const uint64_t* __restrict__ P16, uint32_t status_cap, MsdPlan* __restrict__ plan,
                HeavyCtl* __restrict__ hctl, HeavySeg* __restrict__ hl2) {
+  pdl_entry(true);
   __shared__ uint32_t wsum[kSegs / 32];
   __shared__ uint32_t rmax;
   const uint32_t s = threadIdx.x, lane = s & 31u, warp = s >> 5;
@@ -776,6 +800,7 @@ struct ScatterSmem {
 
 template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterArgs<K> a) {
+  pdl_entry(true);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<ScatterSmem<K, kHasValues>*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -1116,6 +1141,7 @@ template <typename K, bool kHasValues>
 __global__ void k_copy_if_identity(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
                                    uint32_t* __restrict__ vout, uint64_t n, const LsdPlan* __restrict__ plan,
                                    const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!lsd_enabled(msd) || plan->executed != 0) return;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     kout[i] = kin[i];
@@ -1432,6 +1458,7 @@ template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(kLocalThreads, 2)
     k_local_sort(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
                  const MsdPlan* __restrict__ msd, const uint32_t* __restrict__ big, const HeavyCtl* __restrict__ ctl) {
+  pdl_entry(false);
   // (R is the host's key_bits - 16.  A window moved below a common prefix sends
   // every bin to k_heavy_items instead: a loaded R costs ~26 us here at c5 — it
   // takes a register where the kernel parameter is an operand.)
@@ -1465,6 +1492,7 @@ template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(MidCfg::kThreads, 4)
     k_local_mid(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16, int R,
                 const uint32_t* __restrict__ list, const HeavyCtl* __restrict__ ctl, const MsdPlan* __restrict__ msd) {
+  pdl_entry(false);
   if (!__ldg(&msd->use_msd) || __ldg(&msd->rehist)) return;
   const uint32_t nm = __ldg(&ctl->nmid);
   for (uint32_t i = blockIdx.x; i < nm; i += gridDim.x) {
@@ -1601,6 +1629,7 @@ template <typename K, bool kHasValues>
 __global__ void __launch_bounds__(256)
     k_tiny_bins(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16,
                 const uint32_t* __restrict__ list, const HeavyCtl* __restrict__ ctl, const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   constexpr uint32_t kPer = kTinyMax / 32;  // keys per lane
   if (!msd->use_msd || msd->rehist) return;
   const uint32_t nt = ctl->ntiny;
@@ -1734,6 +1763,23 @@ WideLayout layout(uint64_t n, int key_bytes, int key_bits, bool has_values) {
   return L;
 }
 
+// Launch with programmatic stream serialization (FS_WIDE_PDL); the kernel must
+// begin with pdl_entry().
+template <typename... Exp, typename... Act>
+cudaError_t launch(void (*k)(Exp...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = FS_WIDE_PDL ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
+}
+
 template <typename K, bool kHasValues>
 cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int key_bits, void* temp,
                 cudaStream_t s) {
@@ -1797,30 +1843,30 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     auto* vcnt = (uint32_t*)(t + L.vcnt);
     auto* kbits = (unsigned long long*)(t + L.kbits);
     const uint32_t l1w = (uint32_t)(kRadix * L.hgrid);
-    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
-                                                 l1spill, kbits, nullptr);
+    if ((e = launch(k_top16_hist<K>, (unsigned)(L.hgrid), 1024, hsmem, s, kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
+                                                 l1spill, kbits, nullptr)) != cudaSuccess) return e;
     // the window (a common prefix): a decision from the bins, a pass over the
     // keys only if one bin holds them all, and the histogram again only if the
     // window moved (each kernel returns at once otherwise)
-    k_binbits<<<kHistWords / kBinbitsThreads, kBinbitsThreads, 0, s>>>(partials, L.hgrid, kbits,
+    if ((e = launch(k_binbits, (unsigned)(kHistWords / kBinbitsThreads), kBinbitsThreads, 0, s, partials, L.hgrid, kbits,
                                                                         (uint32_t*)(kbits + 4), key_bits, msd,
-                                                                        spill, l1spill, l1w);
-    k_keybits<K><<<(unsigned)sms, 1024, 0, s>>>(kin, n, kbits + 2, (uint32_t*)(kbits + 4) + 1, key_bits, msd, spill,
-                                                l1spill, l1w);
-    k_top16_hist<K><<<L.hgrid, 1024, hsmem, s>>>(kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
-                                                 l1spill, nullptr, msd);
+                                                                        spill, l1spill, l1w)) != cudaSuccess) return e;
+    if ((e = launch(k_keybits<K>, ((unsigned)sms), 1024, 0, s, kin, n, kbits + 2, (uint32_t*)(kbits + 4) + 1, key_bits, msd, spill,
+                                                l1spill, l1w)) != cudaSuccess) return e;
+    if ((e = launch(k_top16_hist<K>, (unsigned)(L.hgrid), 1024, hsmem, s, kin, n, top_shift, L.chunk_tiles * kSTile, partials, spill,
+                                                 l1spill, nullptr, msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_merge_scan(partials, L.hgrid, spill, nullptr, kHistBins, H16, kHistBins, 0, P16, scan_status,
                                (uint32_t*)(scan_status + scan_tiles(kHistBins)), s)) != cudaSuccess)
       return e;
     auto* hctl = (HeavyCtl*)(t + L.hctl);
     const bool list_big = n < kListBigMaxN;  // one CTA per bin is cheaper once most bins are large
-    k_bin_lists<<<kListGrid, kListThreads, 0, s>>>(H16, P16, n, msd, hctl, (HeavySeg*)(t + L.hseg0),
+    if ((e = launch(k_bin_lists, (unsigned)(kListGrid), kListThreads, 0, s, H16, P16, n, msd, hctl, (HeavySeg*)(t + L.hseg0),
                                                    (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
-                                                   (uint32_t*)(t + L.hmid), (uint32_t*)(t + L.hbig), list_big ? 1 : 0);
-    k_msd_plan<<<1, kSegs, 0, s>>>(P16, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hsegl2));
-    k_vseg_counts<<<L.hgrid, 256, 0, s>>>(partials, l1spill, vcnt, msd);
-    k_vseg_scan<<<kRadix / 8, 256, 0, s>>>(vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd);
+                                                   (uint32_t*)(t + L.hmid), (uint32_t*)(t + L.hbig), list_big ? 1 : 0)) != cudaSuccess) return e;
+    if ((e = launch(k_msd_plan, (unsigned)(1), kSegs, 0, s, P16, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hsegl2))) != cudaSuccess) return e;
+    if ((e = launch(k_vseg_counts, (unsigned)(L.hgrid), 256, 0, s, partials, l1spill, vcnt, msd)) != cudaSuccess) return e;
+    if ((e = launch(k_vseg_scan, (unsigned)(kRadix / 8), 256, 0, s, vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(1, s);
     for (int level = 1; level <= 2; ++level) {
@@ -1829,7 +1875,7 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
       sa.shift = key_bits - kRadixBits * level;
       sa.ticket = tickets + 7 + level;
       sa.tag = (unsigned long long)(8 + level) << kTagShift;
-      k_scatter<K, kHasValues><<<sgrid, kSThreads, ssmem, s>>>(sa);
+      if ((e = launch(k_scatter<K, kHasValues>, (unsigned)(sgrid), kSThreads, ssmem, s, sa)) != cudaSuccess) return e;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       phase_event(1 + level, s);
     }
@@ -1857,11 +1903,21 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
         cudaSuccess)
       return e;
     if (hocc < 1) return cudaErrorLaunchOutOfResources;
-    void* hargs[] = {&ha};
-    // Cooperative launch: every CTA co-resident, so the grid barriers are safe.
-    if ((e = cudaLaunchCooperativeKernel((const void*)k_heavy<K, kHasValues>, dim3((unsigned)(hocc * sms)),
-                                         dim3(kHeavyThreads), hargs, (size_t)hvsmem, s)) != cudaSuccess)
-      return e;
+    {  // cooperative launch (every CTA co-resident, so the grid barriers are safe), also PDL
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(hocc * sms));
+      cfg.blockDim = dim3(kHeavyThreads);
+      cfg.dynamicSmemBytes = (size_t)hvsmem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = FS_WIDE_PDL ? 2 : 1;
+      if ((e = cudaLaunchKernelEx(&cfg, k_heavy<K, kHasValues>, ha)) != cudaSuccess) return e;
+    }
     phase_event(4, s);
     // ---- per-bin sorts: the 16-bit bins that fit, then the recursion's items
     constexpr int lsmem = LocalSmemLayout::total;
@@ -1871,24 +1927,24 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     // small inputs: at most n / 65 bins need a CTA, listed by the plan
     const unsigned lgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kMidCap + 1) + 1)
                                     : (unsigned)kHistBins;
-    k_local_sort<K, kHasValues><<<lgrid, kLocalThreads, lsmem, s>>>(
-        kout, vout, P16, key_bits - kTopBits, msd, list_big ? (const uint32_t*)(t + L.hbig) : nullptr, hctl);
-    k_tiny_bins<K, kHasValues><<<(unsigned)(8 * sms), 256, 0, s>>>(kout, vout, P16, (const uint32_t*)(t + L.htiny),
-                                                                   hctl, msd);
+    if ((e = launch(k_local_sort<K, kHasValues>, (unsigned)(lgrid), kLocalThreads, lsmem, s, 
+        kout, vout, P16, key_bits - kTopBits, msd, list_big ? (const uint32_t*)(t + L.hbig) : nullptr, hctl)) != cudaSuccess) return e;
+    if ((e = launch(k_tiny_bins<K, kHasValues>, ((unsigned)(8 * sms)), 256, 0, s, kout, vout, P16, (const uint32_t*)(t + L.htiny),
+                                                                   hctl, msd)) != cudaSuccess) return e;
     constexpr int msmem = LocalLayout<MidCfg>::total;
     if ((e = cudaFuncSetAttribute(k_local_mid<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   msmem)) != cudaSuccess)
       return e;
     const unsigned mgrid = list_big ? (unsigned)std::min<uint64_t>(kHistBins, n / (kTinyMax + 1) + 1)
                                     : (unsigned)(4 * sms);  // large inputs: few mid bins, a persistent loop
-    k_local_mid<K, kHasValues><<<mgrid, MidCfg::kThreads, msmem, s>>>(kout, vout, P16, key_bits - kTopBits,
-                                                                      (const uint32_t*)(t + L.hmid), hctl, msd);
+    if ((e = launch(k_local_mid<K, kHasValues>, (unsigned)(mgrid), MidCfg::kThreads, msmem, s, kout, vout, P16, key_bits - kTopBits,
+                                                                      (const uint32_t*)(t + L.hmid), hctl, msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_heavy_items<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lsmem)) != cudaSuccess)
       return e;
-    k_heavy_items<K, kHasValues><<<(unsigned)(2 * sms), kLocalThreads, lsmem, s>>>(
-        kout, vout, alt_k, alt_v, hctl, (const HeavyItem*)(t + L.hitems), msd);
+    if ((e = launch(k_heavy_items<K, kHasValues>, ((unsigned)(2 * sms)), kLocalThreads, lsmem, s, 
+        kout, vout, alt_k, alt_v, hctl, (const HeavyItem*)(t + L.hitems), msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(5, s);
   }
@@ -1896,8 +1952,8 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
   // ---- LSD path (when MSD was planned: taken only for a common 16-bit prefix; else every kernel returns at once)
   uint64_t hgrid = (n + 511) / 512;
   if (hgrid > (uint64_t)sms * 4) hgrid = (uint64_t)sms * 4;
-  k_digit_hist<K><<<(unsigned)hgrid, 512, 0, s>>>(kin, n, passes, dhist, msd);
-  k_digit_plan<<<1, kRadix, 0, s>>>(dhist, n, passes, lsd, msd);
+  if ((e = launch(k_digit_hist<K>, ((unsigned)hgrid), 512, 0, s, kin, n, passes, dhist, msd)) != cudaSuccess) return e;
+  if ((e = launch(k_digit_plan, (unsigned)(1), kRadix, 0, s, dhist, n, passes, lsd, msd)) != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int ev0 = L.use_msd ? 6 : 1;
   phase_event(ev0, s);
@@ -1907,11 +1963,11 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     sa.shift = p * kRadixBits;
     sa.ticket = tickets + p;
     sa.tag = (unsigned long long)(p + 1) << kTagShift;
-    k_scatter<K, kHasValues><<<sgrid, kSThreads, ssmem, s>>>(sa);
+    if ((e = launch(k_scatter<K, kHasValues>, (unsigned)(sgrid), kSThreads, ssmem, s, sa)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(ev0 + 1 + p, s);
   }
-  k_copy_if_identity<K, kHasValues><<<(unsigned)(sms * 4), 256, 0, s>>>(kin, vin, kout, vout, n, lsd, msd);
+  if ((e = launch(k_copy_if_identity<K, kHasValues>, ((unsigned)(sms * 4)), 256, 0, s, kin, vin, kout, vout, n, lsd, msd)) != cudaSuccess) return e;
   phase_event(ev0 + 1 + passes, s);
   return cudaGetLastError();
 }

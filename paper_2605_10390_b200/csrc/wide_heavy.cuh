@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
   __shared__ uint64_t wsum64[kHeavyWarps];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, d = tid;
   const uint64_t gtid = blockIdx.x * (uint64_t)kHeavyThreads + tid, gthreads = (uint64_t)gridDim.x * kHeavyThreads;
+  pdl_entry(true);
   if (!a.msd->use_msd) return;
   const uint64_t n_al = a.n & ~(uint64_t)3;  // bulk copies never read past this
   if (tid == 0) {
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
     k_heavy_items(K* __restrict__ kout, uint32_t* __restrict__ vout, const K* __restrict__ kalt,
                   const uint32_t* __restrict__ valt, const HeavyCtl* __restrict__ ctl,
                   const HeavyItem* __restrict__ items, const MsdPlan* __restrict__ msd) {
+  pdl_entry(true);
   if (!msd->use_msd) return;
   const uint32_t ni = ctl->nitems;
   HeavyItem nxt;
