@@ -33,4 +33,11 @@ for rnd in range(1):
     torch.cuda.synchronize()
     t = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
     ok = bool((out[1:].to(torch.int32) >= out[:-1].to(torch.int32)).all().item())
-    print(f"{dist:10s} {os.path.basename(path):24s} median {t[len(t)//2]:7.2f} us  min {t[0]:7.2f}  sorted={ok}", flush=True)
+    # back to back: one event pair around 100 calls (as bench.py times its steps)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(100):
+        L.fs_sort_keys_u16(k.data_ptr(), out.data_ptr(), n, 16, temp.data_ptr(), temp.numel(), s)
+    b.record(); torch.cuda.synchronize()
+    b2b = a.elapsed_time(b) * 1e3 / 100
+    print(f"{dist:10s} {os.path.basename(path):24s} median {t[len(t)//2]:7.2f} us  min {t[0]:7.2f}  b2b {b2b:7.2f}  sorted={ok}", flush=True)

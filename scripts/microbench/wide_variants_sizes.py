@@ -31,8 +31,13 @@ for path in sorted(glob.glob(os.path.join(ROOT, "scripts/microbench/variants/*.s
             a.record(); f(); b.record(); ts.append((a, b))
         torch.cuda.synchronize()
         t = statistics.median(x.elapsed_time(y) for x, y in ts)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20): f()
+        b.record(); torch.cuda.synchronize()
+        t2 = a.elapsed_time(b) / 20  # back to back
         kk = ko.view(torch.int64) ^ torch.iinfo(torch.int64).min
         ok = bool((kk[1:] >= kk[:-1]).all().item())
-        line += f"  2^{n.bit_length() - 1}:{t * 1e3:9.1f}us{'' if ok else '(BAD)'}"
+        line += f"  2^{n.bit_length() - 1}:{t * 1e3:8.1f}/{t2 * 1e3:.1f}us{'' if ok else '(BAD)'}"
         del temp
     print(line, flush=True)
