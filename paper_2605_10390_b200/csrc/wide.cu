@@ -34,7 +34,8 @@
 // (2) Stable LSD with 8-bit digits (small n, fewer than 32 varying key bits):
 //     one read builds all digit histograms (k_digit_hist), k_digit_plan scans
 //     them and skips single-bin digits, then one k_scatter (mode 0) per digit;
-//     n <= kSmallSortMax: the same LSD in one CTA's shared memory (k_small_sort).
+//     n <= FS_SMALL_SORT_MSD_MAX (<= kSmallSortMax for key_bits < 32): the same
+//     LSD in one CTA's shared memory (k_small_sort).
 //
 // Choice: the host picks by n and key_bits; then the MSD path is taken unless
 // one 16-bit bin holds every key after the window moved (then the MSD levels
@@ -166,8 +167,11 @@ constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 #ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
 #define FS_TINY_MAX 128
 #endif
+#ifndef FS_SMALL_SORT_MSD_MAX  // one CTA (k_small_sort) up to this many keys when MSD could run
+#define FS_SMALL_SORT_MSD_MAX 10240  // (pairs: 8,192 74 us vs 90 for MSD; 12,000: 105 vs 89)
+#endif
 #ifndef FS_MSD_MIN_N
-#define FS_MSD_MIN_N (1ull << 15)  // below: LSD (4,096 pairs: 87 us vs 132 for MSD; 16,384: equal)
+#define FS_MSD_MIN_N (FS_SMALL_SORT_MSD_MAX + 1ull)
 #endif
 constexpr uint64_t kMsdMinN = FS_MSD_MIN_N;
 constexpr uint32_t kTinyMax = FS_TINY_MAX;
@@ -1510,7 +1514,10 @@ __global__ void __launch_bounds__(MidCfg::kThreads, 4)
 // u16 permutation (warp multisplit ranks, as sort_bin's slow path), keys and
 // values written through the permutation (values gathered from the input).  Eleven launches of the LSD path cost ~80 us of launch
 // latency at 1,000 pairs.
-constexpr int kSmallSortMax = 16384;  // u64 keys: 128 KB + two u16 permutations 64 KB
+#ifndef FS_SMALL_SORT_MAX
+#define FS_SMALL_SORT_MAX 16384
+#endif
+constexpr int kSmallSortMax = FS_SMALL_SORT_MAX;  // u64 keys: 128 KB + two u16 permutations 64 KB
 constexpr int kSmallThreads = 512;
 constexpr int kSmallWarps = kSmallThreads / 32;
 
@@ -1783,13 +1790,15 @@ cudaError_t launch(void (*k)(Exp...), unsigned grid, unsigned block, size_t smem
 template <typename K, bool kHasValues>
 cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint64_t n, int key_bits, void* temp,
                 cudaStream_t s) {
-  if (n <= (uint64_t)kSmallSortMax) {  // one CTA, every pass in shared memory
+  const int kb_eff = key_bits <= 0 || key_bits > (int)(8 * sizeof(K)) ? (int)(8 * sizeof(K)) : key_bits;
+  if (n <= (uint64_t)kSmallSortMax && (n <= (uint64_t)FS_SMALL_SORT_MSD_MAX || kb_eff < 32)) {
+    // one CTA, every pass in shared memory (beyond FS_SMALL_SORT_MSD_MAX keys only where MSD cannot run)
     constexpr int smem = (int)sizeof(SmallSmem<K, kHasValues>);
     cudaError_t e = cudaFuncSetAttribute(k_small_sort<K, kHasValues>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     phase_event(0, s);
     k_small_sort<K, kHasValues><<<1, kSmallThreads, smem, s>>>(
-        kin, vin, kout, vout, (uint32_t)n, key_bits <= 0 || key_bits > (int)(8 * sizeof(K)) ? (int)(8 * sizeof(K)) : key_bits);
+        kin, vin, kout, vout, (uint32_t)n, kb_eff);
     phase_event(1, s);
     return cudaGetLastError();
   }
