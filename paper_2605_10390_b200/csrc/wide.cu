@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(1024)
   set_window(msd, key_bits, ko & kn, ko, spill, l1spill, l1spill_words, &kb_sh);
 }
 
+constexpr uint32_t kVsegSplit = 8;
 // Level-1 digit counts of every chunk: cnt[v][d] = sum of the chunk's 256 leaves
 // under level-8 node d (its partial) + what the chunk spilled there.
 __global__ void __launch_bounds__(256)
@@ -588,10 +589,13 @@ __global__ void __launch_bounds__(256)
                   uint32_t* __restrict__ cnt, const MsdPlan* __restrict__ msd) {
   pdl_entry(true);
   if (!msd->use_msd) return;
-  const uint32_t v = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  // kVsegSplit CTAs per chunk row, 256 / kVsegSplit digits each (one CTA per
+  // row: 24 us of dependent L2 round trips even at small n)
+  const uint32_t v = blockIdx.x / kVsegSplit, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t d0 = (blockIdx.x % kVsegSplit) * (kRadix / kVsegSplit);
   const uint4* row = reinterpret_cast<const uint4*>(partials + (uint64_t)v * kHistWords);
-#pragma unroll 8  // the loads of 8 digits in flight at once
-  for (uint32_t d = warp; d < kRadix; d += 8) {
+#pragma unroll
+  for (uint32_t d = d0 + warp; d < d0 + kRadix / kVsegSplit; d += 8) {
     const uint4 q = __ldcg(row + d * 32 + lane);  // 128 words = 256 leaves
     uint32_t x = (q.x & 0xFFFFu) + (q.x >> 16) + (q.y & 0xFFFFu) + (q.y >> 16) + (q.z & 0xFFFFu) + (q.z >> 16) +
                  (q.w & 0xFFFFu) + (q.w >> 16);
@@ -1633,7 +1637,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 // would cost more than the sort): every key's rank = #keys of the bin below it
 // (ties by arrival), by shuffles; in place (all keys are in registers first).
 template <typename K, bool kHasValues>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     k_tiny_bins(K* __restrict__ keys, uint32_t* __restrict__ vals, const uint64_t* __restrict__ P16,
                 const uint32_t* __restrict__ list, const HeavyCtl* __restrict__ ctl, const MsdPlan* __restrict__ msd) {
   pdl_entry(true);
@@ -1642,28 +1646,53 @@ __global__ void __launch_bounds__(256)
   const uint32_t nt = ctl->ntiny;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nw = gridDim.x * (blockDim.x / 32);
-  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nw) {
-    const uint32_t v = __ldg(list + t);
-    const uint64_t b0 = __ldg(P16 + v);
-    const uint32_t m = (uint32_t)(__ldg(P16 + v + 1) - b0);  // 2..kTinyMax, warp-uniform
-    K k[kPer];
-    uint32_t val[kPer], r[kPer];
+  // The next bin's keys are loaded before the current bin is ranked (a warp
+  // handles several bins in turn: each would otherwise wait for its loads).
+  uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  K k[kPer];
+  uint32_t val[kPer];
+  uint64_t b0 = 0;
+  uint32_t m = 0;
+  auto load = [&](uint32_t tt, K (&kk)[kPer], uint32_t (&vv)[kPer], uint64_t& bb, uint32_t& mm) {
+    mm = 0;
+    if (tt < nt) {
+      const uint32_t v = __ldg(list + tt);
+      bb = __ldg(P16 + v);
+      mm = (uint32_t)(__ldg(P16 + v + 1) - bb);  // 2..kTinyMax, warp-uniform
+    }
 #pragma unroll
     for (uint32_t q = 0; q < kPer; ++q) {
       const uint32_t i = q * 32 + lane;
-      k[q] = i < m ? keys[b0 + i] : K(0);
-      val[q] = (kHasValues && i < m) ? vals[b0 + i] : 0u;
-      r[q] = 0;
+      kk[q] = i < mm ? keys[bb + i] : K(0);
+      vv[q] = (kHasValues && i < mm) ? vals[bb + i] : 0u;
     }
-    for (uint32_t j = 0; j < m; ++j) {
-      K kj = 0;
+  };
+  load(t, k, val, b0, m);
+  for (; t < nt; t += nw) {
+    K kn[kPer];
+    uint32_t vn[kPer];
+    uint64_t bn = 0;
+    uint32_t mn;
+    load(t + nw, kn, vn, bn, mn);
+    uint32_t r[kPer];
 #pragma unroll
-      for (uint32_t q = 0; q < kPer; ++q) {
-        const K x = __shfl_sync(kFull, k[q], j & 31u);
-        if ((j >> 5) == q) kj = x;
+    for (uint32_t q = 0; q < kPer; ++q) r[q] = 0;
+    if (m <= 32) {  // one key per lane
+      for (uint32_t j = 0; j < m; ++j) {
+        const K kj = __shfl_sync(kFull, k[0], j);
+        r[0] += (kj < k[0]) || (kj == k[0] && j < lane);
       }
+    } else {
+      for (uint32_t j = 0; j < m; ++j) {
+        K kj = 0;
 #pragma unroll
-      for (uint32_t q = 0; q < kPer; ++q) r[q] += (kj < k[q]) || (kj == k[q] && j < q * 32 + lane);
+        for (uint32_t q = 0; q < kPer; ++q) {
+          const K x = __shfl_sync(kFull, k[q], j & 31u);
+          if ((j >> 5) == q) kj = x;
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kPer; ++q) r[q] += (kj < k[q]) || (kj == k[q] && j < q * 32 + lane);
+      }
     }
     __syncwarp();
 #pragma unroll
@@ -1674,6 +1703,13 @@ __global__ void __launch_bounds__(256)
       }
     }
     __syncwarp();
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      k[q] = kn[q];
+      val[q] = vn[q];
+    }
+    b0 = bn;
+    m = mn;
   }
 }
 
@@ -1874,7 +1910,7 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
                                                    (HeavyItem*)(t + L.hitems), (uint32_t*)(t + L.htiny),
                                                    (uint32_t*)(t + L.hmid), (uint32_t*)(t + L.hbig), list_big ? 1 : 0)) != cudaSuccess) return e;
     if ((e = launch(k_msd_plan, (unsigned)(1), kSegs, 0, s, P16, (uint32_t)L.status_tiles, msd, hctl, (HeavySeg*)(t + L.hsegl2))) != cudaSuccess) return e;
-    if ((e = launch(k_vseg_counts, (unsigned)(L.hgrid), 256, 0, s, partials, l1spill, vcnt, msd)) != cudaSuccess) return e;
+    if ((e = launch(k_vseg_counts, (unsigned)(L.hgrid * kVsegSplit), 256, 0, s, partials, l1spill, vcnt, msd)) != cudaSuccess) return e;
     if ((e = launch(k_vseg_scan, (unsigned)(kRadix / 8), 256, 0, s, vcnt, L.hgrid, P16, (uint64_t*)(t + L.vbase), msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     phase_event(1, s);
