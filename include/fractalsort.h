@@ -106,7 +106,7 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
 /* ----------------------------------------------------------------------------
  * fs_sort_keys_u32 / fs_sort_keys_u64 — keys-only ascending sort of wider keys.
  * Two schemes with the same (unique) result:
- *  - trie-binned MSD (NEXT-1; n > 10,240 and key_bits >= 32): one read builds the
+ *  - trie-binned MSD (NEXT-1; n > 8,960 and key_bits >= 32): one read builds the
  *    leaf level of a 16-level compressed trie over the top 16 key bits; its
  *    level-8 and level-16 counters bound two stable 8-bit MSD scatters; every
  *    16-bit bin is then sorted by its remaining bits in shared memory (Alg. 5's
@@ -121,7 +121,7 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
  *    phases", §II) with 8-bit digits and one compressed histogram
  *    per digit, all digit histograms in one read pass (config c5's "multi-digit
  *    precision scaling with compressed histograms per digit", ledger 25); a
- *    digit whose histogram has one non-empty bin is skipped.  n <= 10,240 (or
+ *    digit whose histogram has one non-empty bin is skipped.  n <= 8,960 (or
  *    n <= 16,384 with key_bits < 32): the same LSD inside one CTA's shared
  *    memory (one launch).
  * keys_in and keys_out must not overlap.  key_bits: 0 or 1..32 (u32), 0 or

@@ -56,7 +56,7 @@ def sort_keys(keys: torch.Tensor, key_bits: int = 0, out: torch.Tensor | None = 
     uint16 -> fs_sort_keys_u16 (histogram, scan, count-expansion — one 16-CTA cluster
     launch for n <= 2^18, else two kernels; out may be keys);
     uint32/uint64 -> fs_sort_keys_u32/u64 (trie-binned MSD with a per-bin shared-memory sort
-    for n > 10,240 and key_bits >= 32 — oversize bins recurse on the next digits, the window
+    for n > 8,960 and key_bits >= 32 — oversize bins recurse on the next digits, the window
     moves below a common key prefix — else LSD with one compressed histogram per 8-bit digit;
     decided on the device).
     """

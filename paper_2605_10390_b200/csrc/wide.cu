@@ -168,7 +168,7 @@ constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 #define FS_TINY_MAX 128
 #endif
 #ifndef FS_SMALL_SORT_MSD_MAX  // one CTA (k_small_sort) up to this many keys when MSD could run
-#define FS_SMALL_SORT_MSD_MAX 10240  // (pairs: 8,192 74 us vs 90 for MSD; 12,000: 105 vs 89)
+#define FS_SMALL_SORT_MSD_MAX 8960  // (pairs: 8,192 74 us vs 84 for MSD; 10,240: 91 vs 83)
 #endif
 #ifndef FS_MSD_MIN_N
 #define FS_MSD_MIN_N (FS_SMALL_SORT_MSD_MAX + 1ull)

@@ -283,10 +283,10 @@ def test_msd_narrow_effective_keys_take_lsd(cuda):
     _check_pairs(cuda, k)
 
 
-@pytest.mark.parametrize("n", [10_241, 16_384, (1 << 15) - 1, 1 << 15, 50_001, 1 << 18, 700_001, (1 << 21) + 5])
+@pytest.mark.parametrize("n", [8_961, 16_384, (1 << 15) - 1, 1 << 15, 50_001, 1 << 18, 700_001, (1 << 21) + 5])
 @pytest.mark.parametrize("kind", ["uniform", "few", "sorted"])
 def test_msd_small_inputs(cuda, n, kind):
-    """MSD from 10,241 pairs: bins of <= 128 keys sorted by one warp each
+    """MSD from 8,961 pairs: bins of <= 128 keys sorted by one warp each
     (k_tiny_bins), the others by k_local_sort from the plan's list; ties among
     duplicates keep arrival order."""
     k = datagen.gen_u64(n, seed=n % 1013)
@@ -297,10 +297,10 @@ def test_msd_small_inputs(cuda, n, kind):
     _check_pairs(cuda, k)
 
 
-@pytest.mark.parametrize("n", [1, 2, 777, 8192, 10_240, 10_241, 16383, 16384, 16385])
+@pytest.mark.parametrize("n", [1, 2, 777, 8192, 8_960, 8_961, 10_241, 16383, 16384, 16385])
 @pytest.mark.parametrize("key_bits", [13, 31, 32, 64])
 def test_small_single_cta_sort(cuda, n, key_bits):
-    """n <= 10,240 (<= 16,384 with key_bits < 32): the whole LSD in one CTA's shared
+    """n <= 8,960 (<= 16,384 with key_bits < 32): the whole LSD in one CTA's shared
     memory (k_small_sort), incl. digits skipped because every key shares them;
     above, the multi-kernel paths (MSD, or LSD-8 for key_bits < 32)."""
     k = datagen.gen_u64(n, seed=n + key_bits, key_bits=key_bits)
