@@ -196,10 +196,7 @@ def alg5_sort(keys, p, l_b):
     k = _c(keys, np.uint64)
     out = np.empty_like(k)
     n = k.size
-    lg = 0
-    while lg < 64 and (1 << lg) < n:
-        lg += 1
-    l_n = min(p, lg)
+    l_n = trie_depth(n, p)  # the C oracle's own l_n = min(p, ceil(log2 n)), pinned in the tests
     nb = 1 << (l_n - min(l_b, l_n))
     C = np.empty(nb, dtype=np.uint64)
     rc = lib().oracle_alg5_sort(_p(k), n, p, l_b, _p(out), C.ctypes.data)

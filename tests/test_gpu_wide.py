@@ -77,8 +77,10 @@ def test_sort_pairs_all_passes_skipped(cuda):
 
 def test_c5_full_size_invariants(cuda):
     """Config c5 at full size (2^29 pairs) in bench.py's launch configuration:
-    the four invariants pin the unique stable sort; a 2^22 prefix slice is also
-    compared with the oracle element by element."""
+    the four invariants pin the unique stable sort; the first and last ~2^22
+    outputs are also compared with the oracle element by element (the pairs whose
+    key lies below 2^57 / at or above 2^64 - 2^57 are selected from the INPUT and
+    sorted by the oracle; they must be exactly the head / tail of the output)."""
     n = 1 << 29
     k = torch.empty(n, dtype=torch.uint64, device=cuda)
     v = torch.empty(n, dtype=torch.uint32, device=cuda)
@@ -91,6 +93,14 @@ def test_c5_full_size_invariants(cuda):
     del ko, vo, k, v
     torch.cuda.empty_cache()
     assert oracle.check_pairs_index(kin, kout, vout) == 0
+    idx = np.arange(n, dtype=np.uint32)
+    for sel, where in ((kin < np.uint64(1 << 57), "head"), (kin >= np.uint64(2**64 - 2**57), "tail")):
+        ek, ev = oracle.sort_pairs_u64_u32(kin[sel], idx[sel])
+        m = ek.size
+        assert (1 << 21) < m < (1 << 23)
+        gk, gv = (kout[:m], vout[:m]) if where == "head" else (kout[n - m:], vout[n - m:])
+        np.testing.assert_array_equal(gk, ek, err_msg=where)
+        np.testing.assert_array_equal(gv, ev, err_msg=where)
 
 
 # ---------------------------------------------------------------- trie-binned MSD path

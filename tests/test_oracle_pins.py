@@ -174,6 +174,19 @@ def test_alg5_general_matches_numpy(p, l_b, n):
     out, C = oracle.alg5_sort(k, p, l_b)
     np.testing.assert_array_equal(out, np.sort(k))
     assert int(C.sum()) == n
+    # n_bins = 2^(l_n - l_b) (Alg. 5) with l_n = min(p, ceil(log2 n)) from int.bit_length
+    l_n = min(p, (n - 1).bit_length())
+    assert C.size == 1 << (l_n - min(l_b, l_n))
+
+
+@pytest.mark.parametrize("p", [1, 8, 16, 64])
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 2**16 - 1, 2**16, 2**16 + 1, 2**33 + 7])
+def test_trie_depth_is_min_p_ceil_log2_n(n, p):
+    """l_n = min(p, ceil(log2 n)) (§III.B.1): the expected value comes
+    from Python's exact integer bit_length (ceil(log2 n) = (n - 1).bit_length() for n >= 1; 0 for
+    n <= 1, a one-key trie has no levels), so a floor/ceil or power-of-two slip fails here."""
+    want = min(p, (n - 1).bit_length()) if n >= 1 else 0
+    assert oracle.trie_depth(n, p) == want
 
 
 def test_decompose_round_trip():
@@ -225,6 +238,24 @@ def test_checkers_detect_corruption():
     assert oracle.check_pairs_index(k, ko, bad) != 0           # not a permutation
     badk = ko.copy(); badk[-1] = 0
     assert oracle.check_pairs_index(k, badk, vo) != 0          # order / gather
+
+
+def test_checker_gather_clause_alone():
+    """A mutation that only the gather clause kout[j] == kin[vout[j]] can catch (oracle.c,
+    oracle_check_pairs_index): distinct keys (so no stability constraint applies), kout left sorted,
+    and two values swapped (so vout is still a permutation).  A checker without the gather clause
+    passes it; the real one must report the first swapped position."""
+    n = 4_096
+    k = datagen.gen_u64(n, seed=11)
+    assert np.unique(k).size == n
+    v = datagen.iota_u32(n)
+    ko, vo = oracle.sort_pairs_u64_u32(k, v)
+    assert oracle.check_pairs_index(k, ko, vo) == 0
+    for j, jj in ((0, n - 1), (17, 18), (1000, 3000)):
+        bad = vo.copy(); bad[j], bad[jj] = bad[jj], bad[j]
+        assert np.all(ko[1:] > ko[:-1])                              # order holds, no ties
+        assert np.array_equal(np.sort(bad), v)                       # still a permutation
+        assert oracle.check_pairs_index(k, ko, bad) == j + 1         # caught at the first swapped slot
     s = oracle.sort_u16(datagen.gen_u16("uniform", 1000))
     assert oracle.check_nondecreasing_u16(s) == 0
     s[10], s[500] = s[500], s[10]
