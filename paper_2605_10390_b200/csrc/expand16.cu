@@ -29,6 +29,27 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifdef FS_EXPAND_TRACE
+// Debug-only per-CTA timestamps (scripts/microbench/expand_trace.cu builds this
+// file with -DFS_EXPAND_TRACE); compiled out of libfractalsort.so.
+__device__ unsigned long long g_expand_trace[1 << 16][4];
+#define FS_XTRACE(i)                                                          \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < (1u << 16)) {                        \
+      unsigned long long t_;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_expand_trace[blockIdx.x][i] = t_;                                     \
+      unsigned smid_;                                                         \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                      \
+      g_expand_trace[blockIdx.x][3] = smid_;                                  \
+    }                                                                         \
+  } while (0)
+#else
+#define FS_XTRACE(i) \
+  do {               \
+  } while (0)
+#endif
+
 namespace fs {
 namespace {
 
@@ -38,6 +59,9 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kVecPerThread = FS_EXPAND_VPT;                       // max 16-byte vectors per thread
 constexpr int kSliceCap = 4096;                                    // staged P entries
+#ifndef FS_EXPAND_SLICE_STAGE
+#define FS_EXPAND_SLICE_STAGE 1  // two-level prefix: stage whole slices in one round trip (0: search first)
+#endif
 constexpr int kSliceShift = 9;                                     // two-level: 512-bin slices
 constexpr int kNumSlices = 65536 >> kSliceShift;                   // 128
 static_assert(kNumSlices == kHistSlices, "slice layout shared with hist16.cu");
@@ -126,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 8)
   // Programmatic dependent launch: everything above overlaps the producer's tail;
   // P is read only after the producer grid has completed.
   cudaGridDependencySynchronize();
+  FS_XTRACE(0);
 
   if (kTwoLevel) {  // slice bases: exclusive scan of the 128 slice totals
     const uint64_t t = tid < kNumSlices ? __ldcg(slice_tot + tid) : 0ull;
@@ -156,20 +181,48 @@ __global__ void __launch_bounds__(kThreads, 8)
   const uint64_t vec_end = vec0 + tile_vec < nvec ? vec0 + tile_vec : nvec;
   const uint64_t o0 = pos0 + vec0 * 8;  // first global position of the tile
   const uint32_t len = (uint32_t)((vec_end - vec0) * 8);
-  uint64_t v_lo, v_hi;
-  // Coarse grid: the 128 slice starts (two-level: their P values are the bases
-  // already in shared memory) or 256 evenly spaced points of the global P.
-  block_last_le2(Pv, nbins, kTwoLevel ? (uint64_t)1 << kSliceShift : (nbins + kThreads - 1) / kThreads, o0,
-                 o0 + len - 1, v_lo, v_hi);
-  const uint64_t m = v_hi - v_lo + 2;  // P[v_lo .. v_hi+1]
+  uint64_t v_lo = 0, v_hi = 0, m = 0;
   uint4* dst = reinterpret_cast<uint4*>(out_body) + vec0;
-
-  if (m <= (uint64_t)kSliceCap) {
-    for (uint32_t j = tid; j < m; j += kThreads) {
-      const uint64_t p = Pv(v_lo + j);
-      rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
+  bool staged = false;
+  if (kTwoLevel && FS_EXPAND_SLICE_STAGE) {
+    // One L2 round trip: the slices holding the tile's first and last position
+    // follow from the bases in shared memory; all their bins are staged at once
+    // (the bins before the tile stage as 0 and are skipped by the first search).
+    const uint32_t sa = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0) - 1;
+    const uint32_t sb = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0 + len - 1) - 1;
+    const uint32_t nb = (sb - sa + 1) << kSliceShift;
+    if (nb < (uint32_t)kSliceCap) {
+      v_lo = (uint64_t)sa << kSliceShift;
+      m = nb + 1;
+      for (uint32_t j = tid; j < nb; j += kThreads) {
+        const uint64_t p = __ldcg(P + v_lo + j) + base_sh[sa + (j >> kSliceShift)];
+        rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
+      }
+      if (tid == 0) {  // sentinel: P at the first bin of slice sb + 1 (or n)
+        const uint64_t p = base_sh[sb + 1];
+        rel[nb] = p - o0 >= len ? len : (uint32_t)(p - o0);
+      }
+      staged = true;
     }
+  }
+  if (!staged) {
+    // Coarse grid: the 128 slice starts (two-level: their P values are the bases
+    // already in shared memory) or 256 evenly spaced points of the global P.
+    block_last_le2(Pv, nbins, kTwoLevel ? (uint64_t)1 << kSliceShift : (nbins + kThreads - 1) / kThreads, o0,
+                   o0 + len - 1, v_lo, v_hi);
+    m = v_hi - v_lo + 2;  // P[v_lo .. v_hi+1]
+    if (m <= (uint64_t)kSliceCap) {
+      for (uint32_t j = tid; j < m; j += kThreads) {
+        const uint64_t p = Pv(v_lo + j);
+        rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
+      }
+      staged = true;
+    }
+  }
+
+  if (staged) {
     __syncthreads();
+    FS_XTRACE(1);
     const uint32_t hi = (uint32_t)m - 1;  // searches stay below the sentinel rel[m-1] >= len
     uint32_t j = 0;                       // rel[0] = 0: valid start for every position
 #pragma unroll 4
@@ -203,6 +256,8 @@ __global__ void __launch_bounds__(kThreads, 8)
       }
       st_stream_v4(dst + q, make_uint4(packed[0], packed[1], packed[2], packed[3]));
     }
+    __syncthreads();
+    FS_XTRACE(2);
   } else {
     // Very sparse tile (more than kSliceCap bins): search P in L2 per position.
 #pragma unroll 1
