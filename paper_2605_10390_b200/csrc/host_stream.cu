@@ -51,15 +51,32 @@ HostLayout host_layout(uint64_t n, uint64_t batch) {
   return L;
 }
 
+// The copy stream and its 8 events, created on first use and kept for the life
+// of the process: one set per host thread and device (a thread's calls are
+// issued in order, so re-recording an event in a later call is safe -- a wait
+// captures the record current at the time of the wait; calls from other threads
+// use their own set).  No per-call stream or event creation.
+constexpr int kMaxDevices = 64;
 struct Resources {
   cudaStream_t copy = nullptr;
   cudaEvent_t ev[8] = {};
-  ~Resources() {  // destruction is deferred by the driver until queued work completes
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
-    if (copy) cudaStreamDestroy(copy);
-  }
+  bool ready = false;
 };
+thread_local Resources t_res[kMaxDevices];
+
+cudaError_t resources(Resources*& R) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  R = &t_res[dev];
+  if (R->ready) return cudaSuccess;
+  if (!R->copy && (e = cudaStreamCreateWithFlags(&R->copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  for (int i = 0; i < 8; ++i)
+    if (!R->ev[i] && (e = cudaEventCreateWithFlags(&R->ev[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  R->ready = true;
+  return cudaSuccess;
+}
 
 }  // namespace
 }  // namespace fs
@@ -84,51 +101,56 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
   uint64_t* hist = (uint64_t*)(w + L.hist);
   uint64_t* prefix = (uint64_t*)(w + L.prefix);
 
-  Resources R;
-  cudaError_t e = cudaStreamCreateWithFlags(&R.copy, cudaStreamNonBlocking);
-  for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&R.ev[i], cudaEventDisableTiming);
-  if (e != cudaSuccess) return cuda_fail(e, "fs_sort_keys_u16_host: stream/event create");
-  cudaEvent_t* copied = R.ev;       // [2]
-  cudaEvent_t* consumed = R.ev + 2; // [2] slot free again (hist or D2H done)
-  cudaEvent_t* expanded = R.ev + 4; // [2]
-  cudaEvent_t start = R.ev[6];
-  cudaEvent_t done = R.ev[7];
+  Resources* R = nullptr;
+  cudaError_t e = resources(R);
+  if (e != cudaSuccess) return cuda_fail(e, "fs_sort_keys_u16_host: copy stream/event create");
+  cudaEvent_t* copied = R->ev;       // [2]
+  cudaEvent_t* consumed = R->ev + 2; // [2] slot free again (hist or D2H done)
+  cudaEvent_t* expanded = R->ev + 4; // [2]
+  cudaEvent_t start = R->ev[6];
+  cudaEvent_t done = R->ev[7];
+  // On an error after work was queued: order everything later on `stream` after
+  // the copies already queued on the copy stream (nothing is left dangling).
+  auto drain = [&](fs_status st) {
+    if (cudaEventRecord(done, R->copy) == cudaSuccess) cudaStreamWaitEvent(s, done, 0);
+    return st;
+  };
 
   // The copy stream starts after whatever the caller queued earlier on `stream`.
   cudaEventRecord(start, s);
-  cudaStreamWaitEvent(R.copy, start, 0);
+  cudaStreamWaitEvent(R->copy, start, 0);
 
   const uint64_t B = L.batch, nb = (n + B - 1) / B;
   // ---- phase 1: stream batches in, one reused histogram
   for (uint64_t i = 0; i < nb; ++i) {
     const int slot = (int)(i & 1);
     const uint64_t len = (i + 1) * B <= n ? B : n - i * B;
-    if (i >= 2) cudaStreamWaitEvent(R.copy, consumed[slot], 0);
-    e = cudaMemcpyAsync(buf[slot], keys_in_host + i * B, len * 2, cudaMemcpyHostToDevice, R.copy);
-    if (e != cudaSuccess) return cuda_fail(e, "fs_sort_keys_u16_host: H2D");
-    cudaEventRecord(copied[slot], R.copy);
+    if (i >= 2) cudaStreamWaitEvent(R->copy, consumed[slot], 0);
+    e = cudaMemcpyAsync(buf[slot], keys_in_host + i * B, len * 2, cudaMemcpyHostToDevice, R->copy);
+    if (e != cudaSuccess) return drain(cuda_fail(e, "fs_sort_keys_u16_host: H2D"));
+    cudaEventRecord(copied[slot], R->copy);
     cudaStreamWaitEvent(s, copied[slot], 0);
     fs_status st = fs_histogram_u16(buf[slot], len, 16, hist, i > 0, w + L.htemp, L.htemp_bytes, stream);
-    if (st != FS_OK) return st;
+    if (st != FS_OK) return drain(st);
     cudaEventRecord(consumed[slot], s);
   }
   // ---- phase 2: one scan of the merged histogram
   fs_status st = fs_exclusive_scan_u64(hist, prefix, kHistBins, w + L.stemp, L.stemp_bytes, stream);
-  if (st != FS_OK) return st;
+  if (st != FS_OK) return drain(st);
   // ---- phase 3: reconstruct batch by batch and stream out
   for (uint64_t j = 0; j < nb; ++j) {
     const int slot = (int)(j & 1);
     const uint64_t len = (j + 1) * B <= n ? B : n - j * B;
     if (j >= 2) cudaStreamWaitEvent(s, consumed[slot], 0);
     st = fs_expand_u16(prefix, kHistBins, j * B, j * B + len, buf[slot], stream);
-    if (st != FS_OK) return st;
+    if (st != FS_OK) return drain(st);
     cudaEventRecord(expanded[slot], s);
-    cudaStreamWaitEvent(R.copy, expanded[slot], 0);
-    e = cudaMemcpyAsync(keys_out_host + j * B, buf[slot], len * 2, cudaMemcpyDeviceToHost, R.copy);
-    if (e != cudaSuccess) return cuda_fail(e, "fs_sort_keys_u16_host: D2H");
-    cudaEventRecord(consumed[slot], R.copy);
+    cudaStreamWaitEvent(R->copy, expanded[slot], 0);
+    e = cudaMemcpyAsync(keys_out_host + j * B, buf[slot], len * 2, cudaMemcpyDeviceToHost, R->copy);
+    if (e != cudaSuccess) return drain(cuda_fail(e, "fs_sort_keys_u16_host: D2H"));
+    cudaEventRecord(consumed[slot], R->copy);
   }
-  cudaEventRecord(done, R.copy);
+  cudaEventRecord(done, R->copy);
   cudaStreamWaitEvent(s, done, 0);  // synchronising `stream` now implies the output is on the host
   return finish(s, "fs_sort_keys_u16_host");
 }

@@ -3,7 +3,9 @@
 //
 // Two bit-identical schemes (the stable sort is unique, ledger 28):
 //
-// (1) Trie-binned MSD (default for n >= 2^15 and key_bits >= 32).  The paper's
+// (1) Trie-binned MSD (default for n >= FS_MSD_MIN_N = FS_SMALL_SORT_MSD_MAX + 1
+//     = 8,961 keys when key_bits >= 32; below, and up to kSmallSortMax = 16,384
+//     keys when key_bits < 32, the one-CTA LSD k_small_sort).  The paper's
 //     high-precision path (§III.G.3, Alg. 5) bins the keys by
 //     the top levels of the compressed trie and then sorts each bin by its
 //     remaining bits (per-bin radix), with the index array I
@@ -177,7 +179,6 @@ constexpr uint64_t kMsdMinN = FS_MSD_MIN_N;
 constexpr uint32_t kTinyMax = FS_TINY_MAX;
 constexpr int kMidCap = 2048;  // bins of kTinyMax+1 .. 2,048 keys: k_local_mid (smaller CTAs, 4 per SM)
 constexpr uint64_t kListBigMaxN = 1ull << 26;  // below: k_local_sort runs from the plan's list of bins
-  // bins of <= 64 keys: one warp each (k_tiny_bins), not a CTA
 
 struct LsdPlan {
   uint64_t base[kMaxPasses][kRadix];  // exclusive digit offsets
@@ -354,8 +355,11 @@ __global__ void __launch_bounds__(kRadix)
 // MSD: leaf level of the 16-level compressed trie over the top 16 key bits.
 // Same counter layout and overflow protocol as hist16.cu: u16 counters packed
 // two per word; an add whose returned word has a half >= 2^15 exchanges the word
-// with 0 into the u64 spill.  Every add is checked at once, so a counter stays
-// below 2^15 + 32 warps x 64 + 1024 < 65,536.
+// with 0 into the u64 spill.  Every add is checked at once: after a counter
+// crosses 2^15 each thread adds at most one more key to it before exchanging it,
+// and a warp's run add (lane 0) is at most 32 * kPerVec keys (64 for u64, 128 for
+// u32 keys), so a counter stays below 2^15 + 32 warps x 32 * kPerVec + 1024 <
+// 65,536 (static_assert in k_top16_hist).
 constexpr uint32_t kHotMask = 0x80008000u;
 
 // bm (shared): OR / OR-of-complement of the bins that spilled (their counters
@@ -398,6 +402,7 @@ __global__ void __launch_bounds__(1024, 1)
   pdl_entry(true);
   constexpr int kPerVec = 16 / sizeof(K);
   constexpr int kUnroll = 4;
+  static_assert((1u << 15) + 32u * 32u * kPerVec + 1024u < 65536u, "top16 spill bound violated");
   if (msd != nullptr) {
     if (!msd->rehist) return;
     shift = msd->kb - kTopBits;

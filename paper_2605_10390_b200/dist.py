@@ -146,7 +146,8 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         recv = torch.empty(world, dtype=torch.int64, device=dev)
         dist.all_to_all_single(recv, send.to(torch.int64), group=group)
         recv_list = [int(x) for x in recv.tolist()]
-        assert sum(recv_list) == end - begin
+        if sum(recv_list) != end - begin:
+            raise RuntimeError(f"mode A: rank {rank} receives {sum(recv_list)} keys for a range of {end - begin}")
         local_sorted = ops.sort_keys(shard) if shard.numel() else shard
         recv_buf = torch.empty(end - begin, dtype=torch.uint16, device=dev)
         # NCCL/gloo have no 16-bit integer type: exchange bytes.
@@ -247,7 +248,9 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
         gathered_send = [torch.empty_like(send_t) for _ in range(world)]
         dist.all_gather(gathered_send, send_t, group=group)
         all_send = torch.stack(gathered_send).cpu().tolist()       # [source][dest]
-        assert sum(all_send[r][rank] for r in range(world)) == end - begin
+        if sum(all_send[r][rank] for r in range(world)) != end - begin:
+            raise RuntimeError(f"mode P: rank {rank} would receive {sum(all_send[r][rank] for r in range(world))} "
+                               f"pairs for a range of {end - begin}")
         if peers is None:
             peers = (PeerBuffers(dev, group, torch.uint64), PeerBuffers(dev, group, torch.uint32))
         cap = -(-N // world)
@@ -266,7 +269,8 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
     recv_t = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.tolist()]
-    assert sum(recv) == end - begin
+    if sum(recv) != end - begin:
+        raise RuntimeError(f"mode A: rank {rank} receives {sum(recv)} pairs for a range of {end - begin}")
     rk = torch.empty(end - begin, dtype=torch.uint64, device=dev)
     rv = torch.empty(end - begin, dtype=torch.uint32, device=dev)
     # NCCL / gloo have no unsigned 64/32-bit types: exchange the same bytes as int64 / int32
