@@ -28,8 +28,8 @@ $(PKG)/libfractalsort.so: $(KERNEL_OBJS)
 datagen/libfsdatagen.so: datagen/datagen.cu datagen/fsg.h datagen/fsg_rng.h
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -shared -o $@ datagen/datagen.cu
 
-oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
-	$(CC) $(CFLAGS) -shared -o $@ oracle/oracle.c
+oracle/liboracle.so: oracle/oracle.c oracle/oracle_mt.c oracle/oracle.h
+	$(CC) $(CFLAGS) -pthread -shared -o $@ oracle/oracle.c oracle/oracle_mt.c
 
 clean:
 	rm -rf build $(PKG)/libfractalsort.so datagen/libfsdatagen.so oracle/liboracle.so

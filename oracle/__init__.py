@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_check_nondecreasing_u16.restype = u64
         L.oracle_check_pairs_index.argtypes = [vp, u64, vp, vp]
         L.oracle_check_pairs_index.restype = u64
+        L.oracle_sort_u16_mt.argtypes = [vp, u64, vp, i32]
+        L.oracle_sort_u16_mt.restype = i32
         _lib = L
     return _lib
 
@@ -108,6 +110,16 @@ def sort_u16(keys) -> np.ndarray:
     k = _c(keys, np.uint16)
     out = np.empty_like(k)
     lib().oracle_sort_u16(_p(k), k.size, _p(out))
+    return out
+
+
+def sort_u16_mt(keys, threads: int) -> np.ndarray:
+    """The u16 oracle on `threads` POSIX threads (oracle_mt.c) -- timing only."""
+    k = _c(keys, np.uint16)
+    out = np.empty_like(k)
+    rc = lib().oracle_sort_u16_mt(_p(k), k.size, _p(out), int(threads))
+    if rc:
+        raise RuntimeError(f"oracle_sort_u16_mt rc={rc}")
     return out
 
 

@@ -36,6 +36,12 @@ void oracle_reconstruct_counts_u16(const uint64_t* C, uint64_t nbins, uint64_t o
 /* Keys-only ascending sort of u16 keys = histogram then ReconstructAll. */
 void oracle_sort_u16(const uint16_t* keys, uint64_t n, uint16_t* out);
 
+/* The same sort on nthreads POSIX threads (oracle_mt.c), for timing only:
+ * private per-thread histograms, their sum, then every thread reconstructs its
+ * own range of output positions (the paper's local -> global scheme,
+ * PAPER.md:86-92).  Returns 0; 1 if memory is short, 2 if a thread failed. */
+int oracle_sort_u16_mt(const uint16_t* keys, uint64_t n, uint16_t* out, int nthreads);
+
 /* Alg. 1 AddItem with ledger fixes 1-3: every node on the
  * MSB-first root-to-leaf path of each key is incremented once.  levels holds
  * p+1 dense levels (computable pointers): level l has 2^l

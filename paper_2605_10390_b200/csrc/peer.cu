@@ -15,10 +15,15 @@
 //
 // B200 design: the destination buffers are peer mappings (CUDA IPC over
 // NVLink/NVSwitch); each rank streams its n_g keys (2 B each) to their final
-// places — no local sort of the shard, no staging buffer, no all-to-all, no
-// sort of what arrived (Mode A moves 4 + 2 + 2 + 4 B/key through HBM).  Lanes
-// take consecutive j, so a warp's 32 stores are one contiguous 64 B run of a
-// value (split only where a run crosses a rank boundary).
+// places -- no local sort of the shard, no staging buffer, no all-to-all, no
+// sort of what arrived (Mode A moves 4 + 2 + 2 + 4 B/key through HBM).  Rank g's
+// keys of value v form ONE contiguous run of the global output,
+// [P[v] + S_<g[v], P[v] + S_<=g[v]); so the exchange is a set of fills.  Every run
+// is cut into chunks of kChunk keys (and at the owners' range boundaries); a warp
+// fills a chunk with 16-byte stores (v replicated eight times; lanes take
+// consecutive 16 B, so a warp instruction is one 512 B burst over NVLink), the
+// unaligned head and tail of the chunk with 2-byte stores.  The chunk list is the
+// exclusive scan of ceil(C_g[v] / kChunk) (decoupled-lookback scan, scan.cu).
 #include "common.cuh"
 #include "internal.cuh"
 #include "kernels.cuh"
@@ -27,16 +32,17 @@ namespace fs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPerThread = 32;  // positions per thread (strided by the warp width)
+constexpr uint64_t kChunk = 8192;  // keys per chunk (16 KB: 32 store instructions per warp)
 
 FS_DEVINL uint64_t range_begin(uint64_t d, uint64_t G, uint64_t N) {
   return (uint64_t)(((unsigned __int128)N * d) / G);
 }
 
-// tot[v] = sum_r C[r][v], cg[v] = C[g][v], below[v] = sum_{r<g} C[r][v].
+// tot[v] = sum_r C[r][v], cg[v] = C[g][v], below[v] = sum_{r<g} C[r][v],
+// nch[v] = chunks of rank g's run of v.
 __global__ void __launch_bounds__(kThreads)
     k_peer_counts(const uint64_t* __restrict__ C, int G, int g, uint64_t nbins, uint64_t* __restrict__ tot,
-                  uint64_t* __restrict__ cg, uint64_t* __restrict__ below) {
+                  uint64_t* __restrict__ cg, uint64_t* __restrict__ below, uint64_t* __restrict__ nch) {
   const uint64_t v = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
   if (v >= nbins) return;
   uint64_t t = 0, b = 0;
@@ -45,53 +51,67 @@ __global__ void __launch_bounds__(kThreads)
     if (r < g) b += c;
     t += c;
   }
+  const uint64_t c = C[(uint64_t)g * nbins + v];
   tot[v] = t;
-  cg[v] = C[(uint64_t)g * nbins + v];
+  cg[v] = c;
   below[v] = b;
+  nch[v] = (c + kChunk - 1) / kChunk;
 }
 
-// Largest v < nbins with Pg[v] <= j (Pg[0] = 0 <= j).
-FS_DEVINL uint64_t last_le(const uint64_t* Pg, uint64_t nbins, uint64_t j) {
+// Largest v < nbins with CB[v] <= c (CB[0] = 0 <= c).
+FS_DEVINL uint64_t last_le(const uint64_t* CB, uint64_t nbins, uint64_t c) {
   uint64_t lo = 0, hi = nbins;
   while (hi - lo > 1) {
     const uint64_t mid = (lo + hi) >> 1;
-    if (__ldg(Pg + mid) <= j) lo = mid; else hi = mid;
+    if (__ldcg(CB + mid) <= c) lo = mid; else hi = mid;
   }
   return lo;
 }
 
+// dst[0 .. m) = v (one warp): 2-byte stores up to 16-byte alignment, 16-byte
+// stores, 2-byte stores for the tail.
+FS_DEVINL void warp_fill(uint16_t* dst, uint64_t m, uint16_t v, uint32_t lane) {
+  const uint64_t head = min(m, (uint64_t)(((16 - ((uintptr_t)dst & 15)) & 15) >> 1));
+  if (lane < head) dst[lane] = v;
+  const uint64_t nvec = (m - head) >> 3;
+  uint4* body = reinterpret_cast<uint4*>(dst + head);
+  const uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
+  const uint4 q = make_uint4(w, w, w, w);
+  for (uint64_t i = lane; i < nvec; i += 32) st_stream_v4(body + i, q);
+  const uint64_t t0 = head + (nvec << 3);
+  if (t0 + lane < m) dst[t0 + lane] = v;
+}
+
 __global__ void __launch_bounds__(kThreads)
-    k_expand_to_peers(const uint64_t* __restrict__ P, const uint64_t* __restrict__ Pg,
-                      const uint64_t* __restrict__ below, uint64_t nbins, int G, uint16_t* const* __restrict__ dest) {
-  const uint64_t N = __ldg(P + nbins), ng = __ldg(Pg + nbins);
+    k_expand_to_peers(const uint64_t* __restrict__ P, const uint64_t* __restrict__ cg,
+                      const uint64_t* __restrict__ below, const uint64_t* __restrict__ CB, uint64_t nbins, int G,
+                      uint16_t* const* __restrict__ dest) {
+  const uint64_t N = __ldcg(P + nbins), K = __ldcg(CB + nbins);
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t nwarps = (uint64_t)gridDim.x * (kThreads / 32);
-  constexpr uint64_t kChunk = 32 * kPerThread;  // positions per warp chunk
-  for (uint64_t w = (blockIdx.x * (uint64_t)kThreads + threadIdx.x) >> 5; w * kChunk < ng; w += nwarps) {
-    uint64_t j = w * kChunk + lane;
-    if (j >= ng) continue;  // (no warp collectives below)
-    uint64_t v = last_le(Pg, nbins, j);
-    uint64_t run_end = __ldg(Pg + v + 1);
-    uint64_t run_pos = __ldg(P + v) + __ldg(below + v) - __ldg(Pg + v);  // global position = run_pos + j
-    int d = (int)(((unsigned __int128)(run_pos + j) * G) / (N ? N : 1));
+  for (uint64_t c = (blockIdx.x * (uint64_t)kThreads + threadIdx.x) >> 5; c < K; c += nwarps) {
+    const uint64_t v = last_le(CB, nbins, c);
+    const uint64_t i0 = (c - __ldcg(CB + v)) * kChunk;
+    const uint64_t len = min(kChunk, __ldcg(cg + v) - i0);
+    uint64_t q0 = __ldcg(P + v) + __ldcg(below + v) + i0;  // first global position of the chunk
+    const uint64_t q1 = q0 + len;
+    int d = (int)(((unsigned __int128)q0 * G) / (N ? N : 1));
     if (d >= G) d = G - 1;
-    for (int k = 0; k < kPerThread; ++k, j += 32) {
-      if (j >= ng) break;
-      while (j >= run_end) {  // the next non-empty value (runs are long: a short walk)
-        ++v;
-        run_end = __ldg(Pg + v + 1);
-        run_pos = __ldg(P + v) + __ldg(below + v) - __ldg(Pg + v);
-      }
-      const uint64_t pos = run_pos + j;
-      while (d + 1 < G && range_begin(d + 1, G, N) <= pos) ++d;
-      while (d > 0 && range_begin(d, G, N) > pos) --d;
-      dest[d][pos - range_begin(d, G, N)] = (uint16_t)v;
+    while (d + 1 < G && range_begin(d + 1, G, N) <= q0) ++d;
+    while (d > 0 && range_begin(d, G, N) > q0) --d;
+    while (q0 < q1) {  // the pieces of the chunk in consecutive owners' ranges
+      const uint64_t rb = range_begin(d, G, N), re = range_begin(d + 1, G, N);
+      const uint64_t e = q1 < re ? q1 : re;
+      warp_fill(dest[d] + (q0 - rb), e - q0, (uint16_t)v, lane);
+      q0 = e;
+      ++d;
     }
   }
 }
 
 struct PeerLayout {
-  size_t tot = 0, cg = 0, below = 0, P = 0, Pg = 0, scan1 = 0, scan2 = 0, dest = 0, zero_end = 0, total = 0;
+  size_t tot = 0, cg = 0, below = 0, nch = 0, P = 0, CB = 0, scan1 = 0, scan2 = 0, dest = 0, zero_end = 0,
+         total = 0;
 };
 
 PeerLayout peer_layout(uint64_t nbins, int G) {
@@ -108,9 +128,11 @@ PeerLayout peer_layout(uint64_t nbins, int G) {
   off = align_up(off + sizeof(uint64_t) * nbins);
   L.below = off;
   off = align_up(off + sizeof(uint64_t) * nbins);
+  L.nch = off;
+  off = align_up(off + sizeof(uint64_t) * nbins);
   L.P = off;
   off = align_up(off + sizeof(uint64_t) * (nbins + 1));
-  L.Pg = off;
+  L.CB = off;
   off = align_up(off + sizeof(uint64_t) * (nbins + 1));
   L.dest = off;
   off = align_up(off + sizeof(void*) * (size_t)G);
@@ -129,8 +151,9 @@ cudaError_t launch_expand_to_peers(const uint64_t* hist_all, int G, int g, uint6
   auto* tot = (uint64_t*)(t + L.tot);
   auto* cg = (uint64_t*)(t + L.cg);
   auto* below = (uint64_t*)(t + L.below);
+  auto* nch = (uint64_t*)(t + L.nch);
   auto* P = (uint64_t*)(t + L.P);
-  auto* Pg = (uint64_t*)(t + L.Pg);
+  auto* CB = (uint64_t*)(t + L.CB);
   auto* s1 = (unsigned long long*)(t + L.scan1);
   auto* s2 = (unsigned long long*)(t + L.scan2);
   auto* dest = (uint16_t**)(t + L.dest);
@@ -139,17 +162,17 @@ cudaError_t launch_expand_to_peers(const uint64_t* hist_all, int G, int g, uint6
   if ((e = cudaMemcpyAsync(dest, dest_host, sizeof(void*) * (size_t)G, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return e;
   k_peer_counts<<<(unsigned)((nbins + kThreads - 1) / kThreads), kThreads, 0, s>>>(hist_all, G, g, nbins, tot, cg,
-                                                                                 below);
+                                                                                 below, nch);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const uint64_t st = scan_tiles(nbins);
   if ((e = launch_merge_scan(nullptr, 0, nullptr, tot, nbins, nullptr, 0, 0, P, s1, (uint32_t*)(s1 + st), s)) !=
       cudaSuccess)
     return e;
-  if ((e = launch_merge_scan(nullptr, 0, nullptr, cg, nbins, nullptr, 0, 0, Pg, s2, (uint32_t*)(s2 + st), s)) !=
+  if ((e = launch_merge_scan(nullptr, 0, nullptr, nch, nbins, nullptr, 0, 0, CB, s2, (uint32_t*)(s2 + st), s)) !=
       cudaSuccess)
     return e;
-  const unsigned grid = (unsigned)((uint64_t)device_info().sm_count * 8);  // warp-chunk loop covers any n
-  k_expand_to_peers<<<grid, kThreads, 0, s>>>(P, Pg, below, nbins, G, dest);
+  const unsigned grid = (unsigned)((uint64_t)device_info().sm_count * 8);  // the warp loop covers any chunk count
+  k_expand_to_peers<<<grid, kThreads, 0, s>>>(P, cg, below, CB, nbins, G, dest);
   return cudaGetLastError();
 }
 

@@ -111,17 +111,41 @@ def output_range(rank: int, world: int, n_total: int):
     return (n_total * rank) // world, (n_total * (rank + 1)) // world
 
 
+def _own_range_count(hist_all, rank, begin, end) -> int:
+    """How many of rank's keys land in its own output range [begin, end)
+    (lower rank first for equal keys: global position P[v] + S_<rank[v] + j)."""
+    C = hist_all.to("cpu", torch.int64)
+    tot = C.sum(dim=0)
+    P = torch.cumsum(tot, 0) - tot                              # exclusive scan
+    S = C[:rank].sum(dim=0) if rank else torch.zeros_like(tot)
+    lo = P + S                                                  # first global position of rank's keys of v
+    hi = lo + C[rank]
+    return int((torch.clamp(torch.minimum(hi, torch.full_like(hi, end)) - torch.maximum(lo, torch.full_like(lo, begin)),
+                            min=0)).sum().item())
+
+
 def _total_keys(n_local: int, device, group) -> int:
     t = torch.tensor([n_local], dtype=torch.int64, device=device)
     dist.all_reduce(t, group=group)
     return int(t.item())
 
 
-def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, peers=None):
+def _mark(events, name):
+    if events is not None:
+        events[name].record()
+
+
+def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, peers=None, events=None, stats=None):
     """Sort the union of all ranks' shards; returns (this rank's slice of the sorted
     output, (begin, end) global positions of that slice).  mode "P" writes into
     ``peers.buffers(...)`` (a PeerBuffers by default; pass one to reuse the
-    mappings across calls) and returns a view of this rank's buffer."""
+    mappings across calls) and returns a view of this rank's buffer.
+
+    Measurement hooks (bench.py): ``events`` -- a dict with CUDA events "x0" and
+    "x1", recorded on the current stream around the payload exchange (modes A and
+    P: the all-to-all of the key bytes / the expand-to-peers kernel and the
+    barrier after it); ``stats`` -- a dict that receives "sent_bytes", the bytes
+    this rank sends to other ranks."""
     if shard.dtype != torch.uint16 or shard.dim() != 1:
         raise TypeError("shard must be a 1-D uint16 tensor")
     ops = ops or CudaOps()
@@ -150,10 +174,14 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
             raise RuntimeError(f"mode A: rank {rank} receives {sum(recv_list)} keys for a range of {end - begin}")
         local_sorted = ops.sort_keys(shard) if shard.numel() else shard
         recv_buf = torch.empty(end - begin, dtype=torch.uint16, device=dev)
+        if stats is not None:
+            stats["sent_bytes"] = 2 * (sum(send_list) - send_list[rank])
         # NCCL/gloo have no 16-bit integer type: exchange bytes.
+        _mark(events, "x0")
         dist.all_to_all_single(recv_buf.view(torch.uint8), local_sorted.view(torch.uint8),
                                output_split_sizes=[2 * c for c in recv_list],
                                input_split_sizes=[2 * c for c in send_list], group=group)
+        _mark(events, "x1")
         out = ops.sort_keys(recv_buf) if recv_buf.numel() else recv_buf
         return out, (begin, end)
     if mode == "P":
@@ -166,7 +194,11 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         if peers is None:
             peers = PeerBuffers(dev, group)
         dest = peers.buffers(-(-n_total // world))
+        if stats is not None:
+            stats["sent_bytes"] = 2 * (int(hist_all[rank].sum().item()) - _own_range_count(hist_all, rank, begin, end))
+        _mark(events, "x0")
         ops.expand_to_peers(hist_all, rank, dest)
+        _mark(events, "x1")
         ops.synchronize(dev)
         dist.barrier(group=group)                              # every producer has finished writing
         return dest[rank][:end - begin], (begin, end)

@@ -58,6 +58,39 @@ def test_sort_u16_two_hot_bins(cuda):
     np.testing.assert_array_equal(out, oracle.sort_u16(keys))
 
 
+@pytest.mark.parametrize("pattern", ["alternate", "blocks"])
+def test_sort_u16_maximal_contention_spill(cuda, pattern):
+    """Maximal contention on ONE counter word for a long stretch: 2^31 keys
+    (14.5M per CTA, ~220 spill epochs of each half per CTA), every key one of
+    the two bins of one 32-bit word (4242 / 4243), so every shared-memory
+    atomic of all 1024 threads of every CTA hits the same word and no vector is
+    eight equal keys ("alternate"), or runs of 8 equal keys alternate between
+    the two halves so every vector is run-aggregated ("blocks").  White-box:
+    the kernel's u64 spill array (the first 512 KiB of the temp buffer,
+    hist16.cu) must have received the spilled counts of exactly these two bins,
+    and the output must be exact.  The spill bound (static_assert in hist16.cu)
+    is what keeps the packed u16 halves from wrapping here."""
+    from paper_2605_10390_b200 import _lib
+    n = 1 << 31
+    unit = [4242, 4243] if pattern == "alternate" else [4242] * 8 + [4243] * 8
+    keys = torch.tensor(unit, dtype=torch.int16, device=cuda).repeat(n // len(unit)).view(torch.uint16)
+    L = fs.lib()
+    temp = torch.zeros(L.fs_sort_keys_u16_temp_bytes(n), dtype=torch.uint8, device=cuda)
+    out = torch.empty_like(keys)
+    _lib.check(L.fs_sort_keys_u16(keys.data_ptr(), out.data_ptr(), n, 16, temp.data_ptr(), temp.numel(),
+                                  torch.cuda.current_stream().cuda_stream), "fs_sort_keys_u16")
+    torch.cuda.synchronize()
+    half = n // 2
+    assert bool((out[:half].view(torch.int16) == 4242).all().item())
+    assert bool((out[half:].view(torch.int16) == 4243).all().item())
+    spill = temp[: 65536 * 8].view(torch.int64)
+    nz = torch.nonzero(spill).flatten().cpu().tolist()
+    assert set(nz) == {4242, 4243}
+    grid = min(148, torch.cuda.get_device_properties(cuda).multi_processor_count)
+    for b in (4242, 4243):  # all but < 2^15 + 49,407 per CTA went through the spill
+        assert int(spill[b].item()) >= half - grid * 65536
+
+
 @pytest.mark.parametrize("n", [1, 9, 4095, 65536, 100_003, (1 << 18) - 1, 1 << 18, (1 << 18) + 1])
 @pytest.mark.parametrize("dist", ["uniform", "zipf", "const", "sortedswap"])
 def test_sort_u16_one_cluster_path(cuda, n, dist):

@@ -122,6 +122,16 @@ def test_sort_u16_matches_numpy(n, dist):
     np.testing.assert_array_equal(oracle.sort_u16(k), np.sort(k, kind="stable"))
 
 
+@pytest.mark.parametrize("threads", [1, 2, 3, 7, 16])
+@pytest.mark.parametrize("n", [0, 1, 5, 65_537, 1_000_003])
+def test_sort_u16_mt_equals_single_thread(n, threads):
+    """The timing-only multi-threaded oracle (PAPER.md:86-92 local -> global
+    scheme) is pinned to the single-threaded oracle, every distribution."""
+    for dist in ("uniform", "zipf", "sortedswap", "const"):
+        k = datagen.gen_u16(dist, n, seed=n + threads)
+        np.testing.assert_array_equal(oracle.sort_u16_mt(k, threads), oracle.sort_u16(k))
+
+
 def test_histogram_matches_bincount_and_scan_matches_cumsum():
     k = datagen.gen_u16("zipf", 1_000_003, seed=3)
     C = oracle.histogram_u16(k)
