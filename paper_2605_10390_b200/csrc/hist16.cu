@@ -46,6 +46,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -122,17 +123,37 @@ FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
 
 // add8 for skewed inputs: keys equal to the hot key `h` are counted in a
 // register (hc) instead of contending for one shared-memory word.
-FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc) {
+// FS_HIST_REDIRECT: branch-free -- every key still issues its atomic, but a hot
+// key's goes to this thread's private dummy word (dummy_off, bank = lane, always
+// 0) with increment 0, so a warp instruction never serialises on the hot word
+// and no branch splits the warp (round 1 branched around the atomic: 2.4x the
+// instructions of the uniform loop, profiles/r02/ncu_hist_skew.md).
+#ifndef FS_HIST_REDIRECT
+#define FS_HIST_REDIRECT 1
+#endif
+#ifndef FS_HIST_AGG_REDIRECT
+#define FS_HIST_AGG_REDIRECT 0
+#endif
+FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc, uint32_t dummy_off) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   char* base = reinterpret_cast<char*>(sh);
   uint32_t acc = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t x = w[j];
-    if ((x & 0xFFFFu) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
-    else ++hc;
-    if ((x >> 16) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
-    else ++hc;
+    if (FS_HIST_REDIRECT) {
+      const bool pl = (x & 0xFFFFu) == h, ph = (x >> 16) == h;
+      hc += (uint32_t)pl + (uint32_t)ph;
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (pl ? dummy_off : ((x + x) & 0x1FFFCu))),
+                       pl ? 0u : (x & 1u) * 0xFFFFu + 1u);
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (ph ? dummy_off : ((x >> 15) & 0x1FFFCu))),
+                       ph ? 0u : max(x & 0x10000u, 1u));
+    } else {
+      if ((x & 0xFFFFu) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
+      else ++hc;
+      if ((x >> 16) != h) acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
+      else ++hc;
+    }
   }
   return acc;
 }
@@ -152,11 +173,21 @@ FS_DEVINL bool all8_equal(const uint4& v) {
   return (v.x == v.y) & (v.y == v.z) & (v.z == v.w) & ((v.x >> 16) == (v.x & 0xFFFFu));
 }
 
-// Aggregating path for a vector when the warp has runs of equal keys.  Lanes
-// whose 8 keys all equal lane 0's key (or lane 31's: a run boundary inside the
-// warp) are counted by one atomic of 8 * (number of such lanes) <= 256; other
-// all-equal lanes add 8; the rest take the plain path.
-FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill) {
+// Aggregating path for a vector when the warp has runs of equal keys (sorted or
+// constant inputs).  Lanes whose 8 keys all equal lane 0's key ka (or lane 31's
+// kb: a run boundary inside the warp) are counted by one atomic of
+// 8 * (number of such lanes) <= 256; other all-equal lanes add 8.  A lane with
+// mixed keys (a run boundary or an outlier of a nearly sorted input) counts its
+// keys equal to ka / kb in registers and adds each count with one atomic; with
+// FS_HIST_REDIRECT its other keys' atomics are issued as usual and the run
+// keys' go to the thread's dummy word with increment 0 (round 1 issued all 8
+// keys' atomics to the real words: ~7 same-address lanes per instruction).
+// FS_HIST_AGG_REDIRECT is off: it cut the atomic wavefronts of c3c from 37.3 M
+// to 16.6 M but the divergent lanes' extra instructions made the loop
+// issue-bound, 286 -> 384 us (profiles/r02/ncu_hist_skew.md).
+// (A warp-wide reduction of the run-key counts instead -- __reduce_add_sync --
+// was 1.4x slower on constant keys: profiles/r02/u16_variants_redirect.txt.)
+FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill, uint32_t dummy_off) {
   const uint32_t lane = lane_id();
   const bool eq = all8_equal(v);
   const uint32_t k0 = v.x & 0xFFFFu;
@@ -168,9 +199,30 @@ FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill)
   if (((ma | mb) >> lane) & 1u) return;
   if (eq) {
     add_key(sh, k0, 8u, spill);
-  } else if (add8(sh, v) & kHotMask) {
-    recheck8(sh, v, spill);
+    return;
   }
+  if (!FS_HIST_AGG_REDIRECT) {
+    if (add8(sh, v) & kHotMask) recheck8(sh, v, spill);
+    return;
+  }
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  char* base = reinterpret_cast<char*>(sh);
+  uint32_t ca = 0, cb = 0, acc = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t x = w[j], lo = x & 0xFFFFu, hi = x >> 16;
+    const bool la = lo == ka, lb = lo == kb && !la, ha = hi == ka, hb = hi == kb && !ha;
+    ca += (uint32_t)la + (uint32_t)ha;
+    cb += (uint32_t)lb + (uint32_t)hb;
+    const bool pl = la | lb, ph = ha | hb;
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (pl ? dummy_off : ((x + x) & 0x1FFFCu))),
+                     pl ? 0u : (x & 1u) * 0xFFFFu + 1u);
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (ph ? dummy_off : ((x >> 15) & 0x1FFFCu))),
+                     ph ? 0u : max(x & 0x10000u, 1u));
+  }
+  if (ca) add_key(sh, ka, ca, spill);
+  if (cb) add_key(sh, kb, cb, spill);
+  if (acc & kHotMask) recheck8(sh, v, spill);
 }
 
 constexpr int kSliceBins = 512;                    // merge/scan granularity
@@ -201,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   // ---------------- prologue: zero the local tree, the spill array and the flags
 #pragma unroll
   for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
+  sh[kHistWords + tid] = 0;  // dummy words (FS_HIST_REDIRECT)
   for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins + 1; i += gridDim.x * kThreads) a.spill[i] = 0;
   if (tid == 0) s_hot_key = 0xFFFFFFFFu;
   grid.sync();
@@ -227,6 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   constexpr uint64_t kGroupVec = (uint64_t)kUnroll * kThreads;
 #ifndef FS_HIST_CHUNK_ITERS  // scripts/microbench sweeps
 #define FS_HIST_CHUNK_ITERS 8
+#endif
+#ifndef FS_HIST_DYN_DIV
 #define FS_HIST_DYN_DIV 16
 #endif
   constexpr int kChunkIters = FS_HIST_CHUNK_ITERS;
@@ -236,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   const uint64_t nstatic = ngroups - ngroups / FS_HIST_DYN_DIV;
   bool agg = false;
   uint32_t phase = 0;
+  const uint32_t dummy_off = (kHistWords + tid) * 4u;  // this thread's dummy word (bank = lane, stays 0)
   uint32_t hot = 0xFFFFFFFFu, hot_cnt = 0;  // this warp's view of s_hot_key, refreshed every 4th group
   // the whole warp calls this together (warp votes inside)
   auto process_v = [&](uint4 (&v)[kUnroll]) {
@@ -249,12 +305,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     phase = (phase + 1) & 3;
     if (agg) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill);
+      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill, dummy_off);
     } else {
       uint32_t acc = 0;
       if (FS_HIST_HOT && (FS_HIST_HOT_ALWAYS || hot != 0xFFFFFFFFu)) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) acc |= add8_hot(sh, v[u], hot, hot_cnt);
+        for (int u = 0; u < kUnroll; ++u) acc |= add8_hot(sh, v[u], hot, hot_cnt, dummy_off);
       } else {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) acc |= add8(sh, v[u]);
@@ -283,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
       for (int u = 0; u < kUnroll; ++u) cur[u] = nxt[u];
     }
   }
+  FS_TRACE(6);  // (debug trace: thread 0's static groups done)
   {
     unsigned int* work = reinterpret_cast<unsigned int*>(a.spill + kHistBins);
     const uint64_t dyn0 = nstatic * kGroupVec;
@@ -324,8 +381,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
 
   // Flush the local tree: the first step of the two-step merge.
   uint4* dst = reinterpret_cast<uint4*>(a.partials + (uint64_t)blockIdx.x * kHistWords);
+#ifndef FS_HIST_TMA_FLUSH
+#define FS_HIST_TMA_FLUSH 1
+#endif
+  if (FS_HIST_TMA_FLUSH) {
+    // 8 bulk copies of 16 KB (cp.async.bulk, the TMA engine) instead of 32 K
+    // thread stores: the table was written by every thread's atomics (generic
+    // proxy), so all threads fence towards the async proxy before the barrier.
+    fence_proxy_async_smem();
+    __syncthreads();
+    constexpr uint32_t kPiece = kHistWords * 4 / 8;
+    if (tid < 8) {
+      bulk_s2g(reinterpret_cast<char*>(dst) + tid * kPiece, reinterpret_cast<char*>(sh) + tid * kPiece, kPiece);
+      bulk_commit();
+      bulk_wait_all();
+    }
+  } else {
 #pragma unroll
-  for (int j = 0; j < kHistWords / 4 / kThreads; ++j) dst[tid + j * kThreads] = smem_v4[tid + j * kThreads];
+    for (int j = 0; j < kHistWords / 4 / kThreads; ++j) dst[tid + j * kThreads] = smem_v4[tid + j * kThreads];
+  }
   FS_TRACE(3);
   grid.sync();
   FS_TRACE(4);
@@ -439,7 +513,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     __syncthreads();
   }
   FS_TRACE(5);
-  FS_TRACE(6);
 }
 
 }  // namespace
@@ -461,7 +534,7 @@ cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, 
                           uint64_t* slice_tot, int grid, cudaStream_t s) {
   static_assert(kHistWords % (4 * kThreads) == 0, "flush mapping");
   static_assert(kRowGroups * kSliceBins * 4 + 16 * 8 <= kHistWords * 4, "merge smem");
-  constexpr int smem = kHistWords * 4;
+  constexpr int smem = (kHistWords + kThreads) * 4;  // the table + one dummy word per thread
   cudaError_t e = cudaFuncSetAttribute(k_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   HistArgs a;

@@ -55,4 +55,20 @@ FS_DEVINL void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// 1-D bulk copy shared -> global (bulk_group completion).  dst and src 16-byte
+// aligned, bytes a multiple of 16.  The writing threads must have executed
+// fence_proxy_async_smem() and a barrier before this is issued.
+FS_DEVINL void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+FS_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Waits until every committed bulk group of this thread has completed (writes
+// performed), then orders them before this thread's later generic-proxy accesses.
+FS_DEVINL void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 }  // namespace fs

@@ -11,7 +11,7 @@ SRCS="${VARSRC:-$ALL}"
 mkdir -p scripts/microbench/variants
 for spec in "$@"; do
   name="${spec%%:*}"; defs="${spec#*:}"
-  d=build/var_$name; mkdir -p $d
+  d=build/var_$name; rm -rf $d; mkdir -p $d
   for f in $ALL; do
     if [[ " $SRCS " == *" $f "* ]]; then
       nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $defs -dc -o $d/$f.o paper_2605_10390_b200/csrc/$f.cu &
@@ -20,6 +20,7 @@ for spec in "$@"; do
     fi
   done
   wait
+  for f in $SRCS; do [ -f $d/$f.o ] || { echo "variant $name: $f.cu failed to compile" >&2; exit 1; }; done
   nvcc $ARCH -shared -Xcompiler -fPIC -o scripts/microbench/variants/$name.so $d/*.o
   echo built $name
 done

@@ -30,12 +30,12 @@ int main(){
     unsigned long long tr[256][8]; cudaMemcpyFromSymbol(tr, g_hist_trace, sizeof(tr));
     unsigned long long t0=~0ull; for(int c=0;c<G;c++) t0=std::min(t0,tr[c][0]);
     printf("rep %d: event %.1f us\n",rep,ms*1e3);
-    const char* nm[7]={"start","prologue+sync","mainloop end","flush end","sync2","merge end","scan end"};
+    const char* nm[7]={"start","prologue+sync","mainloop end","flush end","sync2","merge+scan end","static end(w0)"};
     for(int i=0;i<7;i++){ std::vector<double> v; for(int c=0;c<G;c++) v.push_back((tr[c][i]-t0)/1e3); std::sort(v.begin(),v.end());
       printf("  %-14s min %7.2f  med %7.2f  max %7.2f us\n",nm[i],v[0],v[v.size()/2],v.back()); }
     if(rep==3){ // per-CTA main-loop duration vs SM id
-      printf("cta smid mainloop_us\n");
-      for(int c=0;c<G;c++) printf("%d %llu %.2f\n", c, tr[c][7], (tr[c][2]-tr[c][1])/1e3);
+      printf("cta smid mainloop_us static_us\n");
+      for(int c=0;c<G;c++) printf("%d %llu %.2f %.2f\n", c, tr[c][7], (tr[c][2]-tr[c][1])/1e3, (tr[c][6]-tr[c][1])/1e3);
     }
   }
   return 0;
