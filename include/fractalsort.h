@@ -207,6 +207,56 @@ fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins,
 fs_status fs_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* queries, uint64_t q, int upper,
                        uint64_t* out, fs_stream_t stream);
 
+/* ----------------------------------------------------------------------------
+ * Distributed pair sort (SURVEY.md §8(e) pairs; NEXT-2, exchange.cu).
+ *
+ * Exact splitters by compressed histograms (PAPER.md:95 Fractal RMW, 168-190
+ * GetIndex; ledger 13, 23): the key K_d at global position s_d = floor(dN/G) is
+ * fixed digit by digit, 16 bits per level, from the all-reduced histograms below.
+ *
+ * fs_histogram16_u64: hist[v] = #{i : ((keys[i] >> shift) & (2^width - 1)) == v}
+ * for v < 2^width (u64 counts, overwritten), 1 <= width <= 16, shift + width
+ * <= 64 -- the level-1 histogram over every key of the shard.  temp:
+ * fs_histogram16_u64_temp_bytes(n) bytes, 256-byte aligned.
+ *
+ * fs_select_bins_u64: appends to out (capacity cap) every key whose digit is one
+ * of bins[0..nb) (device u32, nb <= 64), in no particular order; *count
+ * (device u64) receives the number of such keys (also when above cap: then only
+ * cap are written).  The candidates of the later levels.
+ *
+ * fs_digit_counts_sorted_u64: for an ascending array sorted[0..m) and np
+ * prefixes (device u64), hist[j * 2^width + v] = #{i : (sorted[i] >> shift) ==
+ * (prefixes[j] >> shift) | v}: the histogram of the next digit among the keys
+ * that share prefix j's bits above it (two binary searches per (j, v)).
+ *
+ * The fused exchange (no local sort before it, no staging copy, no all-to-all):
+ * every pair gets a class, 2d for K_{d-1} < key < K_d and 2d + 1 for key == K_d
+ * (the lowest such d; splitters ascending, G - 1 of them on the device); in
+ * class order, stable within a class, owner d's share is one range
+ * [cuts[d], cuts[d+1]).  fs_pair_classes_u64 counts the classes per 2,048-pair
+ * tile, scans them into temp and writes class_tot[2G - 1] (device u64);
+ * fs_pair_scatter_u64_u32 (same temp, same splitters, called after) writes
+ * pair i with class-order index Q, cuts[d] <= Q < cuts[d+1], to
+ * dest_keys[d][bases[d] + Q - cuts[d]] and dest_vals[...] -- dest_*: HOST arrays
+ * of G device pointers (normally peer-mapped via CUDA IPC); cuts (G + 1, from 0
+ * to n, ascending) and bases (G) are HOST arrays.  1 <= G <= 16.  temp:
+ * fs_pair_exchange_temp_bytes(n, G) bytes, 256-byte aligned.
+ * ------------------------------------------------------------------------- */
+size_t fs_histogram16_u64_temp_bytes(uint64_t n);
+fs_status fs_histogram16_u64(const uint64_t* keys, uint64_t n, int shift, int width, uint64_t* hist, void* temp,
+                             size_t temp_bytes, fs_stream_t stream);
+fs_status fs_select_bins_u64(const uint64_t* keys, uint64_t n, int shift, int width, const uint32_t* bins, int nb,
+                             uint64_t* out, uint64_t cap, uint64_t* count, fs_stream_t stream);
+fs_status fs_digit_counts_sorted_u64(const uint64_t* sorted, uint64_t m, const uint64_t* prefixes, int np, int shift,
+                                     int width, uint64_t* hist, fs_stream_t stream);
+size_t fs_pair_exchange_temp_bytes(uint64_t n, int G);
+fs_status fs_pair_classes_u64(const uint64_t* keys, uint64_t n, const uint64_t* splitters, int G, uint64_t* class_tot,
+                              void* temp, size_t temp_bytes, fs_stream_t stream);
+fs_status fs_pair_scatter_u64_u32(const uint64_t* keys, const uint32_t* vals, uint64_t n, const uint64_t* splitters,
+                                  int G, const uint64_t* cuts_host, const uint64_t* bases_host,
+                                  uint64_t* const* dest_keys_host, uint32_t* const* dest_vals_host, void* temp,
+                                  size_t temp_bytes, fs_stream_t stream);
+
 /* fs_expand_to_peers_u16: the fused exchange of the multi-GPU keys-only sort
  * (SURVEY.md §8(f) NEXT-2): rank g writes each of its own keys straight to its
  * final global sorted position, in the output buffer of the rank that owns it.

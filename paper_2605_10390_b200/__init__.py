@@ -21,7 +21,9 @@ from ._lib import FractalSortError, check, lib
 __all__ = [
     "sort_keys", "sort_pairs", "histogram_u16", "exclusive_scan", "expand_u16", "send_counts",
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
-    "histogram_prefix_u16", "expand_prefix_u16", "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie", "trie_pack", "get_item", "get_index", "hist_merge",
+    "histogram_prefix_u16", "expand_prefix_u16", "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie",
+    "trie_pack", "get_item", "get_index", "hist_merge", "histogram16_u64", "select_bins_u64",
+    "digit_counts_sorted_u64", "PairExchange",
 ]
 
 _TEMP_ALIGN = 256
@@ -202,6 +204,87 @@ def bound_u64(sorted_keys: torch.Tensor, queries: torch.Tensor, upper: bool = Fa
         check(lib().fs_bound_u64(sorted_keys.data_ptr(), sorted_keys.numel(), queries.data_ptr(), queries.numel(),
                                  int(bool(upper)), out.data_ptr(), _stream(dev)), "fs_bound_u64")
     return out
+
+
+def histogram16_u64(keys: torch.Tensor, shift: int, width: int = 16) -> torch.Tensor:
+    """int64[2^width]: histogram of the digit (keys >> shift) & (2^width - 1) (fs_histogram16_u64)."""
+    dev = _require_cuda(keys)
+    if keys.dtype != torch.uint64:
+        raise TypeError("histogram16_u64 expects uint64 keys")
+    hist = torch.empty(1 << width, dtype=torch.int64, device=dev)
+    L = lib()
+    with torch.cuda.device(dev):
+        temp = _temp(L.fs_histogram16_u64_temp_bytes(keys.numel()), dev)
+        check(L.fs_histogram16_u64(keys.data_ptr(), keys.numel(), shift, width, hist.data_ptr(), temp.data_ptr(),
+                                   temp.numel(), _stream(dev)), "fs_histogram16_u64")
+    return hist
+
+
+def select_bins_u64(keys: torch.Tensor, shift: int, width: int, bins: list, cap: int) -> torch.Tensor:
+    """The keys whose digit (keys >> shift) & (2^width - 1) is one of `bins`, in no
+    particular order (fs_select_bins_u64); cap must be at least their number."""
+    dev = _require_cuda(keys)
+    b = torch.tensor(list(bins), dtype=torch.int32, device=dev)
+    out = torch.empty(max(int(cap), 1), dtype=torch.uint64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_select_bins_u64(keys.data_ptr(), keys.numel(), shift, width, b.data_ptr(), b.numel(),
+                                       out.data_ptr(), int(cap), count.data_ptr(), _stream(dev)), "fs_select_bins_u64")
+    m = int(count.item())
+    if m > cap:
+        raise ValueError(f"select_bins_u64: {m} keys match, cap {cap}")
+    return out[:m]
+
+
+def digit_counts_sorted_u64(sorted_keys: torch.Tensor, prefixes: list, shift: int, width: int = 16) -> torch.Tensor:
+    """int64[len(prefixes), 2^width]: per prefix, the histogram of the digit at
+    `shift` among the keys sharing the prefix's bits above it (fs_digit_counts_sorted_u64)."""
+    dev = _require_cuda(sorted_keys)
+    np_ = len(prefixes)
+    hist = torch.empty((np_, 1 << width), dtype=torch.int64, device=dev)
+    if np_ == 0:
+        return hist
+    import numpy as np
+    p = torch.from_numpy(np.array(prefixes, dtype=np.uint64).view(np.int64)).to(dev)
+    with torch.cuda.device(dev):
+        check(lib().fs_digit_counts_sorted_u64(sorted_keys.data_ptr(), sorted_keys.numel(), p.data_ptr(), np_,
+                                               shift, width, hist.data_ptr(), _stream(dev)),
+              "fs_digit_counts_sorted_u64")
+    return hist
+
+
+class PairExchange:
+    """The fused partition-to-peer exchange of the distributed pair sort
+    (fs_pair_classes_u64, then fs_pair_scatter_u64_u32 with the same temp)."""
+
+    def __init__(self, keys: torch.Tensor, vals: torch.Tensor, splitters: list, G: int):
+        import numpy as np
+        self.dev = _require_cuda(keys, vals)
+        self.keys, self.vals, self.G = keys, vals, G
+        self.K = torch.from_numpy(np.array(splitters if splitters else [0], dtype=np.uint64).view(np.int64)).to(self.dev)
+        L = lib()
+        self.temp = _temp(L.fs_pair_exchange_temp_bytes(keys.numel(), G), self.dev)
+
+    def classes(self) -> list:
+        """Class totals (2G - 1 counts: class 2d = strictly inside owner d's key range, 2d + 1 = equal to K_d)."""
+        tot = torch.empty(2 * self.G - 1, dtype=torch.int64, device=self.dev)
+        with torch.cuda.device(self.dev):
+            check(lib().fs_pair_classes_u64(self.keys.data_ptr(), self.keys.numel(), self.K.data_ptr(), self.G,
+                                            tot.data_ptr(), self.temp.data_ptr(), self.temp.numel(),
+                                            _stream(self.dev)), "fs_pair_classes_u64")
+        return [int(x) for x in tot.tolist()]
+
+    def scatter(self, cuts: list, bases: list, dest_keys: list, dest_vals: list) -> None:
+        import ctypes
+        G = self.G
+        c = (ctypes.c_uint64 * (G + 1))(*[int(x) for x in cuts])
+        b = (ctypes.c_uint64 * G)(*[int(x) for x in bases])
+        dk = (ctypes.c_void_p * G)(*[t.data_ptr() for t in dest_keys])
+        dv = (ctypes.c_void_p * G)(*[t.data_ptr() for t in dest_vals])
+        with torch.cuda.device(self.dev):
+            check(lib().fs_pair_scatter_u64_u32(self.keys.data_ptr(), self.vals.data_ptr(), self.keys.numel(),
+                                                self.K.data_ptr(), G, c, b, dk, dv, self.temp.data_ptr(),
+                                                self.temp.numel(), _stream(self.dev)), "fs_pair_scatter_u64_u32")
 
 
 def expand_to_peers_u16(hist_all: torch.Tensor, g: int, dest: list) -> None:

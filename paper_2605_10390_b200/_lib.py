@@ -49,6 +49,13 @@ SIGNATURES = {
     "fs_get_item": (_i32, [_vp, _vp, _vp, _i32, _vp, _u64, _u64, _vp, _vp]),
     "fs_get_index": (_i32, [_vp, _vp, _vp, _i32, _vp, _u64, _vp, _vp]),
     "fs_hist_merge_u64": (_i32, [_vp, _vp, _vp, _u64, _vp]),
+    "fs_histogram16_u64_temp_bytes": (_sz, [_u64]),
+    "fs_histogram16_u64": (_i32, [_vp, _u64, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "fs_select_bins_u64": (_i32, [_vp, _u64, _i32, _i32, _vp, _i32, _vp, _u64, _vp, _vp]),
+    "fs_digit_counts_sorted_u64": (_i32, [_vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "fs_pair_exchange_temp_bytes": (_sz, [_u64, _i32]),
+    "fs_pair_classes_u64": (_i32, [_vp, _u64, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "fs_pair_scatter_u64_u32": (_i32, [_vp, _vp, _u64, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
 
 _lib = None

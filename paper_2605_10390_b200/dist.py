@@ -77,6 +77,26 @@ class CudaOps:
         from . import expand_to_peers_u16
         expand_to_peers_u16(hist_all, g, dest)
 
+    def histogram16_u64(self, keys, shift, width):
+        from . import histogram16_u64
+        return histogram16_u64(keys, shift, width)      # int64[2^width]
+
+    def select_bins_u64(self, keys, shift, width, bins, cap):
+        from . import select_bins_u64
+        return select_bins_u64(keys, shift, width, bins, cap)
+
+    def sort_keys_u64(self, keys):
+        from . import sort_keys
+        return sort_keys(keys)
+
+    def digit_counts_sorted_u64(self, sorted_keys, prefixes, shift, width):
+        from . import digit_counts_sorted_u64
+        return digit_counts_sorted_u64(sorted_keys, prefixes, shift, width)   # int64[len, 2^width]
+
+    def pair_exchange(self, keys, vals, splitters, G):
+        from . import PairExchange
+        return PairExchange(keys, vals, splitters, G)
+
     def synchronize(self, device):
         torch.cuda.synchronize(device)
 
@@ -211,27 +231,109 @@ def _u64_tensor(values, device):
     return torch.from_numpy(np.array(values, dtype=np.uint64).view(np.int64)).to(device).view(torch.uint64)
 
 
+def _levels(key_bits: int):
+    """(shift, width) of the digits from the top, 16 bits each (the last one narrower)."""
+    out, hi = [], key_bits
+    while hi > 0:
+        w = min(16, hi)
+        out.append((hi - w, w))
+        hi -= w
+    return out
+
+
+def splitter_level1(H, bounds, shift):
+    """Top digits of the K_d and L_d = #keys below them, from the global level-1 histogram H."""
+    import numpy as np
+    H = np.asarray(H, dtype=np.int64)
+    cum = np.cumsum(H)
+    K, L = [], []
+    for t in bounds:
+        v = int(np.searchsorted(cum, t, side="right"))
+        K.append(v << shift)
+        L.append(int(cum[v] - H[v]))
+    return K, L
+
+
+def splitter_refine(Hl, bounds, K, L, shift):
+    """One more digit of every K_d (in place) from the global histograms Hl[d] of
+    that digit among the keys sharing K_d's digits so far."""
+    import numpy as np
+    Hl = np.asarray(Hl, dtype=np.int64)
+    for j in range(len(bounds)):
+        cj = np.cumsum(Hl[j])
+        v = int(np.searchsorted(cj, bounds[j] - L[j], side="right"))
+        L[j] += int(cj[v] - Hl[j][v])
+        K[j] |= v << shift
+
+
+def pair_cuts(T_all, K, L, bounds, nr):
+    """Every rank's class-order cuts (G + 1 each) of the fused exchange, from all
+    ranks' class totals T_all[r][c] (c = 2d: K_{d-1} < key < K_d; 2d + 1: key ==
+    K_d, lowest d): owner d's share starts inside the tie class of K_{d-1}, after
+    that class's T = s - L ties below the boundary, lower ranks first."""
+    import numpy as np
+    T_all = np.asarray(T_all, dtype=np.int64)
+    world = len(nr)
+    first = [next(i for i in range(world - 1) if K[i] == K[j]) for j in range(world - 1)]
+    cuts_all = []
+    for r in range(world):
+        start = np.concatenate([[0], np.cumsum(T_all[r])])
+        cuts = [0]
+        for j in range(world - 1):
+            c = 2 * first[j] + 1                                    # the tie class of value K_j
+            take = min(max(bounds[j] - L[j] - int(T_all[:r, c].sum()), 0), int(T_all[r, c]))
+            cuts.append(int(start[c]) + take)
+        cuts.append(int(nr[r]))
+        cuts_all.append(cuts)
+    return cuts_all
+
+
+def _exact_splitters(ops, level1_local, candidates, N: int, world: int, key_bits: int, group):
+    """K_d, L_d for every rank boundary s_d = floor(dN/G), d = 1..G-1: K_d is the key
+    of the element at global sorted position s_d and L_d = #keys < K_d over all
+    ranks, found digit by digit from compressed histograms (
+    no sampling, one all-reduce per 16-bit level -- at most 4 for 64-bit keys).
+    level1_local: this rank's int64 histogram of the top digit over all its keys;
+    candidates(bins): this rank's keys whose top digit is in bins, ascending."""
+    levels = _levels(key_bits)
+    bounds = [(N * d) // world for d in range(1, world)]
+    h = level1_local.to(torch.int64).clone()
+    dist.all_reduce(h, group=group)
+    K, L = splitter_level1(h.cpu().numpy(), bounds, levels[0][0])
+    if len(levels) > 1:
+        cand = candidates(sorted({k >> levels[0][0] for k in K}))
+        for shift, width in levels[1:]:
+            hl = ops.digit_counts_sorted_u64(cand, K, shift, width).to(torch.int64)
+            dist.all_reduce(hl, group=group)
+            splitter_refine(hl.cpu().numpy(), bounds, K, L, shift)
+    return K, L
+
+
 def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=None, key_bits: int = 64,
-                       mode: str = "A", peers=None):
+                       mode: str = "P", peers=None):
     """Stable sort of the (u64 key, u32 value) pairs of all ranks (SURVEY.md §8(e)
-    Mode A for pairs): the ranks' shards are contiguous slices of the input in
+    pairs, §8(f) NEXT-2): the ranks' shards are contiguous slices of the input in
     rank order, so the global stable order breaks key ties by (rank, local
     position).  Returns (this rank's slice of the sorted pairs, (begin, end)).
 
-    1. stable local sort of the shard;
-    2. exact splitters, no sampling: for every rank boundary s_d = floor(dN/G)
-       the key K_d of the element at global position s_d is found by bisection
-       over the key space, each step one fs_bound_u64 (rank counts) and one
-       all_reduce; ties at K_d are split by source rank (ledger 13, 23);
-    3. the payload exchange by those cuts: mode "A" all_to_all of keys and
-       values (NCCL); mode "P" (NEXT-2) every rank stores its slices straight
-       into the owners' receive buffers, mapped with CUDA IPC (peer copies over
-       NVLink, no staging), at offsets from one all_gather of the send counts;
-    4. stable local sort of what arrived (runs arrive in source-rank order).
+    Exact splitters, no sampling (_exact_splitters): K_d at every rank boundary
+    s_d = floor(dN/G) from one all-reduced 16-bit histogram per level; the ties
+    at K_d below the boundary, T_d = s_d - L_d, are split by source rank, then
+    local order (ledger 13, 23).
+    mode "P" (fused exchange, the default): no local sort first -- every pair is
+    classified against the splitters (fs_pair_classes_u64: one all_gather of the
+    2G - 1 class totals gives every rank's cuts) and stored straight into its
+    owner's CUDA-IPC-mapped receive buffer (fs_pair_scatter_u64_u32, peer stores
+    over NVLink); each owner then sorts what arrived, once.
+    mode "A" (payload all-to-all): stable local sort, cuts from the sorted shard,
+    NCCL all_to_all of keys and values, stable local sort of what arrived.
     ``peers``: (keys, values) PeerBuffers to reuse across calls (mode "P").
     """
+    import numpy as np
     if keys.dtype != torch.uint64 or vals.dtype != torch.uint32 or keys.numel() != vals.numel():
         raise TypeError("uint64 keys and uint32 values of equal length expected")
+    if not 1 <= key_bits <= 64:
+        raise ValueError("key_bits must be in 1..64")
     ops = ops or CudaOps()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -240,64 +342,66 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
     sizes = torch.tensor([n_local], dtype=torch.int64, device=dev)
     all_sizes = [torch.empty_like(sizes) for _ in range(world)]
     dist.all_gather(all_sizes, sizes, group=group)
-    N = int(sum(int(t.item()) for t in all_sizes))
+    nr = [int(t.item()) for t in all_sizes]
+    N = sum(nr)
     begin, end = output_range(rank, world, N)
-    ks, vs = ops.sort_pairs(keys, vals) if n_local else (keys, vals)
     if world == 1:
-        return (ks, vs), (begin, end)
+        return (ops.sort_pairs(keys, vals) if n_local else (keys, vals)), (begin, end)
+    shift1, width1 = _levels(key_bits)[0]
     bounds = [(N * d) // world for d in range(1, world)]       # s_d, d = 1 .. G-1
-    lo = [0] * (world - 1)
-    hi = [(1 << key_bits) - 1] * (world - 1)
-    while any(l < h for l, h in zip(lo, hi)):
-        mid = [l + (h - l) // 2 for l, h in zip(lo, hi)]
-        cnt = ops.bound_u64(ks, _u64_tensor(mid, dev), True)     # local #keys <= mid
-        dist.all_reduce(cnt, group=group)
-        c = [int(x) for x in cnt.tolist()]
-        for d in range(world - 1):
-            if lo[d] < hi[d]:
-                if c[d] <= bounds[d]:
-                    lo[d] = mid[d] + 1
-                else:
-                    hi[d] = mid[d]
-    K = _u64_tensor(lo, dev)
-    below = ops.bound_u64(ks, K, False)                          # local #keys < K_d
-    equal = ops.bound_u64(ks, K, True) - below                   # local #keys == K_d
-    mine = torch.stack([below, equal])                           # 2 x (G-1)
-    gathered = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(gathered, mine, group=group)
-    allb = torch.stack(gathered).cpu().tolist()                 # [rank][below/equal][d]
-    cuts = [0]
-    for d in range(world - 1):
-        L = sum(allb[r][0][d] for r in range(world))
-        t = bounds[d] - L                                        # ties at K_d before the boundary
-        before = sum(allb[r][1][d] for r in range(rank))
-        take = min(max(t - before, 0), allb[rank][1][d])
-        cuts.append(allb[rank][0][d] + take)
-    cuts.append(n_local)
-    send = [cuts[d + 1] - cuts[d] for d in range(world)]
-    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
     if mode == "P":
-        gathered_send = [torch.empty_like(send_t) for _ in range(world)]
-        dist.all_gather(gathered_send, send_t, group=group)
-        all_send = torch.stack(gathered_send).cpu().tolist()       # [source][dest]
-        if sum(all_send[r][rank] for r in range(world)) != end - begin:
-            raise RuntimeError(f"mode P: rank {rank} would receive {sum(all_send[r][rank] for r in range(world))} "
-                               f"pairs for a range of {end - begin}")
+        level1 = ops.histogram16_u64(keys, shift1, width1)
+
+        def candidates(bins):
+            cap = int(level1[torch.tensor(bins, dtype=torch.int64, device=level1.device)].sum().item())
+            c = ops.select_bins_u64(keys, shift1, width1, bins, cap)
+            return ops.sort_keys_u64(c) if c.numel() else c
+        K, L = _exact_splitters(ops, level1, candidates, N, world, key_bits, group)
+        ex = ops.pair_exchange(keys, vals, K, world)
+        tot = torch.tensor(ex.classes(), dtype=torch.int64, device=dev)
+        gathered = [torch.empty_like(tot) for _ in range(world)]
+        dist.all_gather(gathered, tot, group=group)
+        T_all = np.stack([t.cpu().numpy() for t in gathered]).astype(np.int64)   # [rank][class]
+        cuts_all = pair_cuts(T_all, K, L, bounds, nr)
+        cuts = cuts_all[rank]
+        if any(cuts[d] > cuts[d + 1] for d in range(world)):
+            raise RuntimeError(f"mode P: rank {rank} cuts not ascending: {cuts}")
+        recv = sum(cuts_all[r][rank + 1] - cuts_all[r][rank] for r in range(world))
+        if recv != end - begin:
+            raise RuntimeError(f"mode P: rank {rank} would receive {recv} pairs for a range of {end - begin}")
+        bases = [sum(cuts_all[r][d + 1] - cuts_all[r][d] for r in range(rank)) for d in range(world)]
         if peers is None:
             peers = (PeerBuffers(dev, group, torch.uint64), PeerBuffers(dev, group, torch.uint32))
         cap = -(-N // world)
         pk, pv = peers[0].buffers(cap), peers[1].buffers(cap)
-        for d in range(world):
-            if send[d]:
-                off = sum(all_send[r][d] for r in range(rank))       # lower ranks first (stable)
-                pk[d][off:off + send[d]].copy_(ks[cuts[d]:cuts[d + 1]], non_blocking=True)
-                pv[d][off:off + send[d]].copy_(vs[cuts[d]:cuts[d + 1]], non_blocking=True)
+        ex.scatter(cuts, bases, pk, pv)
         ops.synchronize(dev)
         dist.barrier(group=group)                                   # every producer has finished writing
         rk, rv = pk[rank][:end - begin], pv[rank][:end - begin]
         if rk.numel():
             rk, rv = ops.sort_pairs(rk, rv)
         return (rk, rv), (begin, end)
+    if mode != "A":
+        raise ValueError(f"unknown mode {mode!r}")
+    ks, vs = ops.sort_pairs(keys, vals) if n_local else (keys, vals)
+    level1 = ops.digit_counts_sorted_u64(ks, [0], shift1, width1)[0]
+    K, L = _exact_splitters(ops, level1, lambda bins: ks, N, world, key_bits, group)
+    Kt = _u64_tensor(K, dev)
+    below = ops.bound_u64(ks, Kt, False)                         # local #keys < K_d
+    equal = ops.bound_u64(ks, Kt, True) - below                  # local #keys == K_d
+    mine = torch.stack([below, equal])                           # 2 x (G-1)
+    gathered = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(gathered, mine, group=group)
+    allb = torch.stack(gathered).cpu().tolist()                 # [rank][below/equal][d]
+    cuts = [0]
+    for d in range(world - 1):
+        t = bounds[d] - L[d]                                     # ties at K_d before the boundary
+        before = sum(allb[r][1][d] for r in range(rank))
+        take = min(max(t - before, 0), allb[rank][1][d])
+        cuts.append(allb[rank][0][d] + take)
+    cuts.append(n_local)
+    send = [cuts[d + 1] - cuts[d] for d in range(world)]
+    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
     recv_t = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.tolist()]

@@ -92,6 +92,62 @@ class OracleOps:
         return torch.from_numpy(np.searchsorted(sorted_keys.numpy(), queries.numpy(),
                                                 side="right" if upper else "left").astype(np.int64))
 
+    # -- the distributed pair sort's splitter levels and fused exchange, by definition
+    def histogram16_u64(self, keys, shift, width):
+        d = (keys.numpy() >> np.uint64(shift)) & np.uint64((1 << width) - 1)
+        return torch.from_numpy(np.bincount(d.astype(np.int64), minlength=1 << width).astype(np.int64))
+
+    def select_bins_u64(self, keys, shift, width, bins, cap):
+        k = keys.numpy()
+        d = (k >> np.uint64(shift)) & np.uint64((1 << width) - 1)
+        sel = k[np.isin(d, np.array(bins, dtype=np.uint64))]
+        assert sel.size <= cap
+        return torch.from_numpy(sel.copy())
+
+    def sort_keys_u64(self, keys):
+        import oracle
+        return torch.from_numpy(oracle.sort_keys_u64(keys.numpy()))
+
+    def digit_counts_sorted_u64(self, sorted_keys, prefixes, shift, width):
+        hi = sorted_keys.numpy() >> np.uint64(shift)
+        out = np.zeros((len(prefixes), 1 << width), dtype=np.int64)
+        for j, p in enumerate(prefixes):
+            t = (np.uint64(p) >> np.uint64(shift)) | np.arange(1 << width, dtype=np.uint64)
+            out[j] = np.searchsorted(hi, t, side="right") - np.searchsorted(hi, t, side="left")
+        return torch.from_numpy(out)
+
+    def pair_exchange(self, keys, vals, splitters, G):
+        return _OracleExchange(keys, vals, splitters, G)
+
+
+class _OracleExchange:
+    """fs_pair_classes_u64 / fs_pair_scatter_u64_u32 by their definition: class 2d for
+    K_{d-1} < key < K_d, 2d + 1 for key == K_d (lowest d); class order stable; pair with
+    class-order index Q in [cuts[d], cuts[d+1]) goes to dest[d][bases[d] + Q - cuts[d]]."""
+
+    def __init__(self, keys, vals, splitters, G):
+        k = keys.numpy()
+        K = np.array(splitters, dtype=np.uint64)
+        d = np.searchsorted(K, k, side="left")
+        tie = np.zeros(k.size, dtype=bool)
+        inside = d < K.size
+        tie[inside] = K[d[inside]] == k[inside]
+        self.cls = 2 * d + tie
+        self.k, self.v, self.G = k, vals.numpy(), G
+
+    def classes(self):
+        return np.bincount(self.cls, minlength=2 * self.G - 1).astype(np.int64).tolist()
+
+    def scatter(self, cuts, bases, dest_keys, dest_vals):
+        order = np.argsort(self.cls, kind="stable")
+        Q = np.arange(order.size)
+        owner = np.searchsorted(np.array(cuts), Q, side="right") - 1
+        for dd in range(self.G):
+            sel = owner == dd
+            slots = np.array(bases[dd]) + Q[sel] - cuts[dd]
+            dest_keys[dd].numpy()[slots] = self.k[order[sel]]
+            dest_vals[dd].numpy()[slots] = self.v[order[sel]]
+
 
 class SharedPeers:
     """CPU stand-in of dist.PeerBuffers: shared-memory buffers made by the parent."""
@@ -177,7 +233,8 @@ def test_output_range_helper():
 
 
 PAIR_CASES = [("uniform", False, "A"), ("ties8", True, "A"), ("const", False, "A"), ("ties3", True, "A"),
-              ("uniform", True, "P"), ("ties8", False, "P"), ("const", True, "P")]
+              ("uniform", True, "P"), ("ties8", False, "P"), ("const", True, "P"), ("ties3", False, "P"),
+              ("hi16", True, "P"), ("hi16", False, "A")]
 N_PAIRS = 20_011
 
 
@@ -190,6 +247,8 @@ def pair_input(kind):
         k = (k % np.uint64(3)) << np.uint64(62)
     elif kind == "const":
         k = np.full(N_PAIRS, 0xFEDCBA9876543210, dtype=np.uint64)
+    elif kind == "hi16":              # every key in one top-16 bin: the later levels decide
+        k = (k & np.uint64((1 << 48) - 1)) | np.uint64(0xBEEF << 48)
     return k, datagen.iota_u32(N_PAIRS)
 
 
@@ -216,9 +275,12 @@ def pair_worker(rank, world, port, outdir, peer_bufs):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_distributed_pairs_match_oracle(tmp_path, world):
-    """Pairs, modes A (all_to_all) and P (stores into the owners' buffers): exact
-    splitters by bisection + tie split by source rank, exchange, stable local re-sort.  The concatenated slices equal the oracle's
-    stable sort of the whole input (values = arrival indices: stability checked)."""
+    """Pairs, modes A (local sort, all_to_all, local sort) and P (classes, stores into
+    the owners' buffers, one sort): exact splitters from one all-reduced 16-bit
+    histogram per level, tie split by source rank.  The concatenated slices equal
+    the oracle's stable sort of the whole input (values = arrival indices:
+    stability checked), for uniform keys, few distinct keys whose ties straddle
+    every boundary, constant keys and keys sharing their top 16 bits."""
     import oracle
     cap = -(-N_PAIRS // world)
     peer_bufs = [([torch.zeros(cap, dtype=torch.int64).view(torch.uint64).share_memory_() for _ in range(world)],

@@ -96,3 +96,75 @@ def test_two_level_prefix_sum_over_ranks(cuda, dist_name):
     want = oracle.sort_u16(keys)
     for a, b in [(0, keys.size), (0, 1), (12345, 1_234_567), (keys.size - 9, keys.size)]:
         np.testing.assert_array_equal(fs.expand_prefix_u16(p2, a, b).cpu().numpy(), want[a:b])
+
+
+def _virtual_pair_sort(cuda, k, v, G, cuts_in, key_bits=64):
+    """The distributed pair sort of dist.sort_pairs_u64_u32 mode "P" for G virtual
+    ranks on one GPU: the collectives become host sums, every other step is the
+    library's (fs_histogram16_u64, fs_select_bins_u64, fs_sort_keys_u64,
+    fs_digit_counts_sorted_u64, fs_pair_classes_u64, fs_pair_scatter_u64_u32 into
+    G separate owner buffers, fs_sort_pairs_u64_u32 per owner)."""
+    import paper_2605_10390_b200 as fs
+    from paper_2605_10390_b200 import dist as fsd
+    N = k.size
+    shards = [(torch.from_numpy(k[cuts_in[r]:cuts_in[r + 1]].copy()).to(cuda),
+               torch.from_numpy(v[cuts_in[r]:cuts_in[r + 1]].copy()).to(cuda)) for r in range(G)]
+    nr = [cuts_in[r + 1] - cuts_in[r] for r in range(G)]
+    levels = fsd._levels(key_bits)
+    bounds = [(N * d) // G for d in range(1, G)]
+    (s1, w1) = levels[0]
+    h1 = [fs.histogram16_u64(sk, s1, w1) for sk, _ in shards]
+    K, L = fsd.splitter_level1(sum(h.cpu().numpy() for h in h1), bounds, s1)
+    bins = sorted({x >> s1 for x in K})
+    cands = []
+    for (sk, _), h in zip(shards, h1):
+        cap = int(h[torch.tensor(bins, device=cuda)].sum().item())
+        c = fs.select_bins_u64(sk, s1, w1, bins, cap)
+        cands.append(fs.sort_keys(c) if c.numel() else c)
+    for shift, width in levels[1:]:
+        Hl = sum(fs.digit_counts_sorted_u64(c, K, shift, width).cpu().numpy() for c in cands)
+        fsd.splitter_refine(Hl, bounds, K, L, shift)
+    exs = [fs.PairExchange(sk, sv, K, G) for sk, sv in shards]
+    T_all = np.array([ex.classes() for ex in exs], dtype=np.int64)
+    cuts_all = fsd.pair_cuts(T_all, K, L, bounds, nr)
+    owners = [(N * d) // G for d in range(G + 1)]
+    dk = [torch.empty(owners[d + 1] - owners[d], dtype=torch.uint64, device=cuda) for d in range(G)]
+    dv = [torch.empty(owners[d + 1] - owners[d], dtype=torch.uint32, device=cuda) for d in range(G)]
+    for r, ex in enumerate(exs):
+        bases = [sum(cuts_all[q][d + 1] - cuts_all[q][d] for q in range(r)) for d in range(G)]
+        ex.scatter(cuts_all[r], bases, dk, dv)
+    torch.cuda.synchronize()
+    outk, outv = [], []
+    for d in range(G):
+        if dk[d].numel():
+            a, b = fs.sort_pairs(dk[d], dv[d])
+            outk.append(a.cpu().numpy())
+            outv.append(b.cpu().numpy())
+    return np.concatenate(outk), np.concatenate(outv), K
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("kind", ["uniform", "ties8", "const", "hi16", "ties3"])
+def test_fused_pair_exchange_virtual_ranks(cuda, G, kind):
+    """NEXT-2 for pairs on one GPU: exact splitters from the CUDA histogram levels,
+    the classes + peer-store scatter into G owner buffers, one stable sort per
+    owner; the owners' outputs concatenate to the oracle's stable sort (values =
+    arrival indices, so stability is checked)."""
+    n = 300_007
+    k = datagen.gen_u64(n, seed=G)
+    if kind == "ties8":
+        k = k & np.uint64(7)
+    elif kind == "const":
+        k = np.full(n, 0x0123456789ABCDEF, dtype=np.uint64)
+    elif kind == "hi16":
+        k = (k & np.uint64((1 << 48) - 1)) | np.uint64(0xBEEF << 48)
+    elif kind == "ties3":
+        k = (k % np.uint64(3)) << np.uint64(62)
+    v = datagen.iota_u32(n)
+    cuts = [0] + sorted((n * (2 * r + 1)) // (2 * G) for r in range(1, G)) + [n]  # uneven shards
+    gk, gv, K = _virtual_pair_sort(cuda, k, v, G, cuts)
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(gk, ek)
+    np.testing.assert_array_equal(gv, ev)
+    # the splitters are exactly the keys at the rank boundaries
+    assert K == [int(ek[(n * d) // G]) for d in range(1, G)]
