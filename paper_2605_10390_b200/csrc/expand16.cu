@@ -144,15 +144,36 @@ __global__ void __launch_bounds__(kThreads, 8)
                uint64_t tail_n, uint16_t* __restrict__ out, uint32_t vpt_rt) {
   const uint32_t vpt = kVpt ? (uint32_t)kVpt : vpt_rt;
   __shared__ uint32_t rel[kSliceCap];
+  __shared__ uint32_t zeros_sh;
   __shared__ uint64_t base_sh[kNumSlices + 1];
-  __shared__ uint64_t wtot[kThreads / 32];
   const uint32_t tid = threadIdx.x;
   // Programmatic dependent launch: everything above overlaps the producer's tail;
   // P is read only after the producer grid has completed.
   cudaGridDependencySynchronize();
   FS_XTRACE(0);
+  if (threadIdx.x == 0) zeros_sh = 0;  // (first read after the setup's barriers)
 
-  if (kTwoLevel) {  // slice bases: exclusive scan of the 128 slice totals
+#ifndef FS_EXPAND_WARP_SETUP
+#define FS_EXPAND_WARP_SETUP 0
+#endif
+  if (kTwoLevel && FS_EXPAND_WARP_SETUP) {  // slice bases: exclusive scan of the 128 slice totals, by warp 0
+    if (tid < 32) {
+      uint64_t t[4], run = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] = __ldcg(slice_tot + tid * 4 + i);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) run += t[i];
+      uint64_t ex = warp_inclusive_scan<uint64_t>(run) - run;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        base_sh[tid * 4 + i] = ex;
+        ex += t[i];
+      }
+      if (tid == 31) base_sh[kNumSlices] = ex;
+    }
+    __syncthreads();
+  } else if (kTwoLevel) {  // slice bases: exclusive scan of the 128 slice totals (4 warps)
+    __shared__ uint64_t wtot[kThreads / 32];
     const uint64_t t = tid < kNumSlices ? __ldcg(slice_tot + tid) : 0ull;
     const uint64_t inc = warp_inclusive_scan<uint64_t>(t);
     if ((tid & 31) == 31) wtot[tid >> 5] = inc;
@@ -167,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 8)
     if (tid == 0) base_sh[kNumSlices] = all;
     __syncthreads();
   }
+  static_assert(kNumSlices == 4 * 32, "warp 0 scans the slice totals four per lane");
   const PrefixView<kTwoLevel> Pv{P, base_sh, nbins};
 
   // Unaligned head/tail keys (< 8 each): one per thread in CTA 0.
@@ -188,16 +210,35 @@ __global__ void __launch_bounds__(kThreads, 8)
     // One L2 round trip: the slices holding the tile's first and last position
     // follow from the bases in shared memory; all their bins are staged at once
     // (the bins before the tile stage as 0 and are skipped by the first search).
-    const uint32_t sa = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0) - 1;
-    const uint32_t sb = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0 + len - 1) - 1;
+    uint32_t sa, sb;
+    if (FS_EXPAND_WARP_SETUP) {  // every warp finds them itself from the bases (ballots), no block barrier
+      const uint32_t lane = tid & 31u;
+      uint32_t ca = 0, cbn = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t b = base_sh[lane * 4 + i];
+        ca += __popc(__ballot_sync(kFull, b <= o0));
+        cbn += __popc(__ballot_sync(kFull, b <= o0 + len - 1));
+      }
+      sa = ca - 1;
+      sb = cbn - 1;
+    } else {
+      sa = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0) - 1;
+      sb = (uint32_t)__syncthreads_count(tid < kNumSlices && base_sh[tid] <= o0 + len - 1) - 1;
+    }
     const uint32_t nb = (sb - sa + 1) << kSliceShift;
     if (nb < (uint32_t)kSliceCap) {
       v_lo = (uint64_t)sa << kSliceShift;
       m = nb + 1;
+      uint32_t z = 0;
       for (uint32_t j = tid; j < nb; j += kThreads) {
         const uint64_t p = __ldcg(P + v_lo + j) + base_sh[sa + (j >> kSliceShift)];
         rel[j] = p <= o0 ? 0u : (p - o0 >= len ? len : (uint32_t)(p - o0));
+        z += p <= o0;
       }
+      // the bins before the tile stage as 0 (a prefix): every thread's search
+      // starts at the last of them instead of at 0
+      if (z) atomicAdd(&zeros_sh, z);
       if (tid == 0) {  // sentinel: P at the first bin of slice sb + 1 (or n)
         const uint64_t p = base_sh[sb + 1];
         rel[nb] = p - o0 >= len ? len : (uint32_t)(p - o0);
@@ -224,7 +265,10 @@ __global__ void __launch_bounds__(kThreads, 8)
     __syncthreads();
     FS_XTRACE(1);
     const uint32_t hi = (uint32_t)m - 1;  // searches stay below the sentinel rel[m-1] >= len
-    uint32_t j = 0;                       // rel[0] = 0: valid start for every position
+#ifndef FS_EXPAND_ZSTART
+#define FS_EXPAND_ZSTART 1
+#endif
+    uint32_t j = FS_EXPAND_ZSTART && zeros_sh ? zeros_sh - 1 : 0;  // rel[j] = 0: a valid start for every position
 #pragma unroll 4
     for (uint32_t k = 0; k < vpt; ++k) {
       const uint32_t q = k * kThreads + tid;
