@@ -138,7 +138,10 @@ FS_DEVINL void block_last_le2(const View& P, uint64_t nbins, uint64_t cs, uint64
 // kVpt: vectors per thread, fixed at compile time (16) for large outputs; 0 means
 // the runtime value `vpt` (small outputs, smaller tiles).
 template <bool kTwoLevel, int kVpt>
-__global__ void __launch_bounds__(kThreads, 8)
+#ifndef FS_EXPAND_MINB
+#define FS_EXPAND_MINB 8  // CTAs per SM the register budget is sized for (32 registers)
+#endif
+__global__ void __launch_bounds__(kThreads, FS_EXPAND_MINB)
     k_expand16(const uint64_t* __restrict__ P, const uint64_t* __restrict__ slice_tot, uint64_t nbins, uint64_t pos0,
                uint64_t nvec, uint16_t* __restrict__ out_body, uint64_t out_begin, uint64_t head, uint64_t tail_pos,
                uint64_t tail_n, uint16_t* __restrict__ out, uint32_t vpt_rt) {
