@@ -9,6 +9,8 @@
 
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fractalsort.h"
 #include "internal.cuh"
 #include "kernels.cuh"
@@ -20,10 +22,34 @@ namespace {
 thread_local char g_err[512] = "";
 thread_local void* const* g_events = nullptr;
 thread_local int g_nevents = 0;
+thread_local int g_nvtx_depth = 0;         // public calls in progress on this thread (nesting)
+thread_local bool g_nvtx_phase_open = false;
+const char* const kPhaseNames[] = {"phase 0", "phase 1", "phase 2",  "phase 3",  "phase 4",  "phase 5",
+                                   "phase 6", "phase 7", "phase 8",  "phase 9",  "phase 10", "phase 11",
+                                   "phase 12", "phase 13", "phase 14", "phase 15", "phase 16"};
+}  // namespace
+
+NvtxScope::NvtxScope(const char* name) {
+  if (g_nvtx_depth++ == 0) g_nvtx_phase_open = false;
+  nvtxRangePushA(name);
+}
+
+NvtxScope::~NvtxScope() {
+  if (g_nvtx_depth == 1 && g_nvtx_phase_open) {
+    nvtxRangePop();
+    g_nvtx_phase_open = false;
+  }
+  nvtxRangePop();
+  --g_nvtx_depth;
 }
 
 void phase_event(int i, cudaStream_t s) {
   if (g_events && i >= 0 && i < g_nevents && g_events[i]) cudaEventRecord((cudaEvent_t)g_events[i], s);
+  if (g_nvtx_depth == 1 && i >= 0 && i < (int)(sizeof(kPhaseNames) / sizeof(kPhaseNames[0]))) {
+    if (g_nvtx_phase_open) nvtxRangePop();
+    nvtxRangePushA(kPhaseNames[i]);
+    g_nvtx_phase_open = true;
+  }
 }
 
 fs_status fail(fs_status s, const char* fmt, ...) {
@@ -147,7 +173,7 @@ size_t fs_sort_pairs_u64_u32_temp_bytes(uint64_t n, int key_bits) {
 
 fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t n, int key_bits, void* temp,
                            size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (key_bits < 0 || key_bits > 16) return fail(FS_ERR_INVALID_ARGUMENT, "key_bits %d not in 0..16", key_bits);
   if (n == 0) return FS_OK;
   if (!keys_in || !keys_out || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer with n > 0");
@@ -189,7 +215,7 @@ fs_status fs_sort_keys_u16(const uint16_t* keys_in, uint16_t* keys_out, uint64_t
 
 fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint64_t* hist, int accumulate,
                            void* temp, size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (key_bits < 0 || key_bits > 16) return fail(FS_ERR_INVALID_ARGUMENT, "key_bits %d not in 0..16", key_bits);
   if (!hist) return fail(FS_ERR_INVALID_ARGUMENT, "hist is NULL");
   const uint64_t nb = (uint64_t)1 << (key_bits ? key_bits : 16);
@@ -220,7 +246,7 @@ fs_status fs_histogram_u16(const uint16_t* keys, uint64_t n, int key_bits, uint6
 
 fs_status fs_histogram_prefix_u16(const uint16_t* keys, uint64_t n, uint64_t* prefix2, void* temp, size_t temp_bytes,
                                   fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (!prefix2) return fail(FS_ERR_INVALID_ARGUMENT, "prefix2 is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) {
@@ -246,7 +272,7 @@ fs_status fs_histogram_prefix_u16(const uint16_t* keys, uint64_t n, uint64_t* pr
 
 fs_status fs_expand_prefix_u16(const uint64_t* prefix2, uint64_t out_begin, uint64_t out_end, uint16_t* out,
                                fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (out_end < out_begin) return fail(FS_ERR_INVALID_ARGUMENT, "out_end < out_begin");
   if (out_end == out_begin) return FS_OK;
   if (!prefix2 || !out) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -261,7 +287,7 @@ fs_status fs_expand_prefix_u16(const uint64_t* prefix2, uint64_t out_begin, uint
 
 fs_status fs_exclusive_scan_u64(const uint64_t* hist, uint64_t* prefix, uint64_t nbins, void* temp,
                                 size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (nbins == 0 || nbins > (1ull << 32)) return fail(FS_ERR_INVALID_ARGUMENT, "nbins %llu not in 1..2^32",
                                                      (unsigned long long)nbins);
   if (!hist || !prefix || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -285,7 +311,7 @@ fs_status fs_exclusive_scan_u64(const uint64_t* hist, uint64_t* prefix, uint64_t
 
 fs_status fs_expand_u16(const uint64_t* prefix, uint64_t nbins, uint64_t out_begin, uint64_t out_end,
                         uint16_t* out, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (nbins == 0 || nbins > 65536) return fail(FS_ERR_INVALID_ARGUMENT, "nbins %llu not in 1..65536",
                                               (unsigned long long)nbins);
   if (out_end < out_begin) return fail(FS_ERR_INVALID_ARGUMENT, "out_end < out_begin");
@@ -302,7 +328,7 @@ fs_status fs_expand_u16(const uint64_t* prefix, uint64_t nbins, uint64_t out_beg
 
 fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint64_t* send,
                          fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (G < 1 || G > 1024 || g < 0 || g >= G) return fail(FS_ERR_INVALID_ARGUMENT, "bad G=%d g=%d", G, g);
   if (nbins == 0 || nbins > 65536) return fail(FS_ERR_INVALID_ARGUMENT, "nbins not in 1..65536");
   if (!hist_all || !send) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -316,7 +342,7 @@ fs_status fs_send_counts(const uint64_t* hist_all, int G, int g, uint64_t nbins,
 
 fs_status fs_bound_u64(const uint64_t* sorted, uint64_t n, const uint64_t* queries, uint64_t q, int upper,
                        uint64_t* out, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (q == 0) return FS_OK;
   if (!queries || !out || (n && !sorted)) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (upper != 0 && upper != 1) return fail(FS_ERR_INVALID_ARGUMENT, "upper must be 0 or 1");
@@ -335,7 +361,7 @@ size_t fs_expand_to_peers_u16_temp_bytes(uint64_t nbins, int G) {
 
 fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest,
                                  void* temp, size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (G < 1 || G > 1024 || g < 0 || g >= G) return fail(FS_ERR_INVALID_ARGUMENT, "bad G=%d g=%d", G, g);
   if (nbins == 0 || nbins > 65536) return fail(FS_ERR_INVALID_ARGUMENT, "nbins not in 1..65536");
   if (!hist_all || !dest || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -354,7 +380,7 @@ fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_
 size_t fs_trie_levels_count(int p) { return (p < 1 || p > 24) ? 0 : (((size_t)2 << p) - 1); }
 
 fs_status fs_trie_levels(const uint64_t* leaf_hist, int p, uint64_t* levels, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
   if (!leaf_hist || !levels) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (overlaps(leaf_hist, ((size_t)1 << p) * 8, levels, fs_trie_levels_count(p) * 8))
@@ -389,7 +415,7 @@ size_t fs_trie_pack_temp_bytes(int p) { return (p < 1 || p > 24) ? 0 : align_up(
 fs_status fs_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min_width, int32_t* widths,
                        uint64_t* bit_offsets, uint64_t* packed, uint64_t packed_words, void* temp,
                        size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
   if (min_width < 1 || min_width > 64) return fail(FS_ERR_INVALID_ARGUMENT, "min_width %d not in 1..64", min_width);
   if (!levels || !widths || !bit_offsets || !packed || !temp) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -406,7 +432,7 @@ fs_status fs_trie_pack(const uint64_t* levels, int p, uint64_t capacity, int min
 fs_status fs_get_item(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
                       const uint64_t* ranks, uint64_t q, uint64_t default_value, uint64_t* items,
                       fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
   if (q == 0) return FS_OK;
   if (!widths || !bit_offsets || !packed || !ranks || !items) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -418,7 +444,7 @@ fs_status fs_get_item(const int32_t* widths, const uint64_t* bit_offsets, const 
 
 fs_status fs_get_index(const int32_t* widths, const uint64_t* bit_offsets, const uint64_t* packed, int p,
                        const uint64_t* values, uint64_t q, uint64_t* indices, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (p < 1 || p > 24) return fail(FS_ERR_INVALID_ARGUMENT, "p %d not in 1..24", p);
   if (q == 0) return FS_OK;
   if (!widths || !bit_offsets || !packed || !values || !indices)
@@ -431,7 +457,7 @@ fs_status fs_get_index(const int32_t* widths, const uint64_t* bit_offsets, const
 
 fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t count,
                             fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (count == 0) return FS_OK;
   if (!a || !b || !out) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -443,7 +469,7 @@ fs_status fs_hist_merge_u64(const uint64_t* a, const uint64_t* b, uint64_t* out,
 static fs_status wide_sort(const char* name, const void* kin, const uint32_t* vin, void* kout, uint32_t* vout,
                            uint64_t n, int key_bytes, int key_bits, void* temp, size_t temp_bytes,
                            fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   const int width = key_bytes * 8;
   if (key_bits < 0 || key_bits > width) return fail(FS_ERR_INVALID_ARGUMENT, "%s: key_bits %d not in 0..%d", name,
                                                     key_bits, width);
@@ -489,7 +515,7 @@ fs_status fs_sort_pairs_u64_u32(const uint64_t* keys_in, const uint32_t* vals_in
                                 uint32_t* vals_out, uint64_t n, int key_bits, void* temp, size_t temp_bytes,
                                 fs_stream_t stream) {
   if (n && (!vals_in || !vals_out)) {
-    clear_error();
+    FS_ENTRY();
     return fail(FS_ERR_INVALID_ARGUMENT, "fs_sort_pairs_u64_u32: NULL values with n > 0");
   }
   return wide_sort("fs_sort_pairs_u64_u32", keys_in, vals_in, keys_out, vals_out, n, 8, key_bits, temp,

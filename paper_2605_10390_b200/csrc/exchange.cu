@@ -317,7 +317,7 @@ size_t fs_histogram16_u64_temp_bytes(uint64_t n) {
 
 fs_status fs_histogram16_u64(const uint64_t* keys, uint64_t n, int shift, int width, uint64_t* hist, void* temp,
                              size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (width < 1 || width > 16 || shift < 0 || shift + width > 64)
     return fail(FS_ERR_INVALID_ARGUMENT, "digit [shift %d, +%d) outside a u64 key or wider than 16 bits", shift,
                 width);
@@ -353,7 +353,7 @@ fs_status fs_histogram16_u64(const uint64_t* keys, uint64_t n, int shift, int wi
 
 fs_status fs_select_bins_u64(const uint64_t* keys, uint64_t n, int shift, int width, const uint32_t* bins, int nb,
                              uint64_t* out, uint64_t cap, uint64_t* count, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (width < 1 || width > 16 || shift < 0 || shift + width > 64)
     return fail(FS_ERR_INVALID_ARGUMENT, "digit [shift %d, +%d) outside a u64 key or wider than 16 bits", shift,
                 width);
@@ -375,7 +375,7 @@ fs_status fs_select_bins_u64(const uint64_t* keys, uint64_t n, int shift, int wi
 
 fs_status fs_digit_counts_sorted_u64(const uint64_t* sorted, uint64_t m, const uint64_t* prefixes, int np, int shift,
                                      int width, uint64_t* hist, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (width < 1 || width > 16 || shift < 0 || shift + width > 64)
     return fail(FS_ERR_INVALID_ARGUMENT, "digit [shift %d, +%d) outside a u64 key or wider than 16 bits", shift,
                 width);
@@ -394,7 +394,7 @@ size_t fs_pair_exchange_temp_bytes(uint64_t n, int G) { return class_layout(n, G
 
 fs_status fs_pair_classes_u64(const uint64_t* keys, uint64_t n, const uint64_t* splitters, int G, uint64_t* class_tot,
                               void* temp, size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (G < 1 || G > kMaxG) return fail(FS_ERR_INVALID_ARGUMENT, "G %d not in 1..%d", G, kMaxG);
   if (!class_tot || !temp || (n && !keys) || (G > 1 && !splitters))
     return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -425,7 +425,7 @@ fs_status fs_pair_scatter_u64_u32(const uint64_t* keys, const uint32_t* vals, ui
                                   int G, const uint64_t* cuts_host, const uint64_t* bases_host,
                                   uint64_t* const* dest_keys_host, uint32_t* const* dest_vals_host, void* temp,
                                   size_t temp_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (G < 1 || G > kMaxG) return fail(FS_ERR_INVALID_ARGUMENT, "G %d not in 1..%d", G, kMaxG);
   if (!cuts_host || !bases_host || !dest_keys_host || !dest_vals_host || !temp || (n && (!keys || !vals)) ||
       (G > 1 && !splitters))

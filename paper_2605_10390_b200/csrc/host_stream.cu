@@ -89,7 +89,7 @@ size_t fs_sort_keys_u16_host_work_bytes(uint64_t n, uint64_t batch) { return hos
 
 fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out_host, uint64_t n, uint64_t batch,
                                 void* work, size_t work_bytes, fs_stream_t stream) {
-  clear_error();
+  FS_ENTRY();
   if (n == 0) return FS_OK;
   if (!keys_in_host || !keys_out_host || !work) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer with n > 0");
   if ((uintptr_t)work & 255) return fail(FS_ERR_INVALID_ARGUMENT, "work not 256-byte aligned");

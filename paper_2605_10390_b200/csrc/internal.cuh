@@ -22,6 +22,19 @@ fs_status fail(fs_status s, const char* fmt, ...);
 fs_status cuda_fail(cudaError_t e, const char* where);
 fs_status finish(cudaStream_t s, const char* where);
 void clear_error();
+
+// NVTX ranges (header-only nvtx3: free unless a profiler is attached): one range
+// per public call, named after it, and inside it one range per phase of the
+// call (opened at every phase boundary, see phase_event).
+struct NvtxScope {
+  explicit NvtxScope(const char* name);
+  ~NvtxScope();
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+#define FS_ENTRY()   \
+  ::fs::clear_error(); \
+  ::fs::NvtxScope fs_nvtx_scope_(__func__)
 bool overlaps(const void* a, size_t an, const void* b, size_t bn);
 // Records phase event i on stream s if fs_set_phase_events armed one (thread-local).
 void phase_event(int i, cudaStream_t s);
