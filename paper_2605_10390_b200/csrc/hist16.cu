@@ -131,9 +131,6 @@ FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
 #ifndef FS_HIST_REDIRECT
 #define FS_HIST_REDIRECT 1
 #endif
-#ifndef FS_HIST_AGG_REDIRECT
-#define FS_HIST_AGG_REDIRECT 0
-#endif
 FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc, uint32_t dummy_off) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   char* base = reinterpret_cast<char*>(sh);
@@ -176,18 +173,15 @@ FS_DEVINL bool all8_equal(const uint4& v) {
 // Aggregating path for a vector when the warp has runs of equal keys (sorted or
 // constant inputs).  Lanes whose 8 keys all equal lane 0's key ka (or lane 31's
 // kb: a run boundary inside the warp) are counted by one atomic of
-// 8 * (number of such lanes) <= 256; other all-equal lanes add 8.  A lane with
-// mixed keys (a run boundary or an outlier of a nearly sorted input) counts its
-// keys equal to ka / kb in registers and adds each count with one atomic; with
-// FS_HIST_REDIRECT its other keys' atomics are issued as usual and the run
-// keys' go to the thread's dummy word with increment 0 (round 1 issued all 8
-// keys' atomics to the real words: ~7 same-address lanes per instruction).
-// FS_HIST_AGG_REDIRECT is off: it cut the atomic wavefronts of c3c from 37.3 M
-// to 16.6 M but the divergent lanes' extra instructions made the loop
-// issue-bound, 286 -> 384 us (profiles/r02/ncu_hist_skew.md).
-// (A warp-wide reduction of the run-key counts instead -- __reduce_add_sync --
-// was 1.4x slower on constant keys: profiles/r02/u16_variants_redirect.txt.)
-FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill, uint32_t dummy_off) {
+// 8 * (number of such lanes) <= 256; other all-equal lanes add 8; a lane with
+// mixed keys (a run boundary or an outlier of a nearly sorted input) takes the
+// plain path.  (Taking its keys equal to ka / kb out of the atomics -- the
+// hot-key redirect -- cut c3c's atomic wavefronts from 37.3 M to 16.6 M but the
+// divergent lanes' extra instructions made the loop issue-bound: 286 -> 384 us,
+// 334 us with ka alone; a warp-wide __reduce_add_sync of the run counts: constant
+// keys 192 -> 277 us.  profiles/r02/u16_variants_redirect.txt,
+// u16_variants_agg_redirect_lean.txt.)
+FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill) {
   const uint32_t lane = lane_id();
   const bool eq = all8_equal(v);
   const uint32_t k0 = v.x & 0xFFFFu;
@@ -201,28 +195,7 @@ FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill,
     add_key(sh, k0, 8u, spill);
     return;
   }
-  if (!FS_HIST_AGG_REDIRECT) {
-    if (add8(sh, v) & kHotMask) recheck8(sh, v, spill);
-    return;
-  }
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  char* base = reinterpret_cast<char*>(sh);
-  uint32_t ca = 0, cb = 0, acc = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t x = w[j], lo = x & 0xFFFFu, hi = x >> 16;
-    const bool la = lo == ka, lb = lo == kb && !la, ha = hi == ka, hb = hi == kb && !ha;
-    ca += (uint32_t)la + (uint32_t)ha;
-    cb += (uint32_t)lb + (uint32_t)hb;
-    const bool pl = la | lb, ph = ha | hb;
-    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (pl ? dummy_off : ((x + x) & 0x1FFFCu))),
-                     pl ? 0u : (x & 1u) * 0xFFFFu + 1u);
-    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (ph ? dummy_off : ((x >> 15) & 0x1FFFCu))),
-                     ph ? 0u : max(x & 0x10000u, 1u));
-  }
-  if (ca) add_key(sh, ka, ca, spill);
-  if (cb) add_key(sh, kb, cb, spill);
-  if (acc & kHotMask) recheck8(sh, v, spill);
+  if (add8(sh, v) & kHotMask) recheck8(sh, v, spill);
 }
 
 constexpr int kSliceBins = 512;                    // merge/scan granularity
@@ -305,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     phase = (phase + 1) & 3;
     if (agg) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill, dummy_off);
+      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill);
     } else {
       uint32_t acc = 0;
       if (FS_HIST_HOT && (FS_HIST_HOT_ALWAYS || hot != 0xFFFFFFFFu)) {
