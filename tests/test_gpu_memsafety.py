@@ -218,3 +218,59 @@ def test_repeated_sorts_bit_identical(cuda):
     for _ in range(8):
         ok, ov = fs.sort_pairs(kp, vp)
         assert torch.equal(ok, rk) and torch.equal(ov, rv)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties"])
+def test_pair_exchange_guards(cuda, kind):
+    """The fused pair exchange (fs_pair_classes_u64 + fs_pair_scatter_u64_u32) writes
+    only inside every owner's share (G = 3 virtual ranks, each destination guarded
+    and misaligned), whatever its temp holds; the owners' buffers hold exactly the
+    pairs the class-order cuts assign them."""
+    import ctypes
+    L = fs.lib()
+    n, G = 200_003, 3
+    k = datagen.gen_u64(n, seed=17)
+    if kind == "ties":
+        k = k & np.uint64(3)
+    v = datagen.iota_u32(n)
+    order = np.argsort(k, kind="stable")
+    K = [int(k[order[(n * d) // G]]) for d in range(1, G)]
+    Kd = torch.from_numpy(np.array(K, dtype=np.uint64).view(np.int64)).to(cuda)
+    kd, vd = torch.from_numpy(k).to(cuda), torch.from_numpy(v).to(cuda)
+    tb = L.fs_pair_exchange_temp_bytes(n, G)
+    # classes and cuts by definition (one rank: ties split at the boundary positions)
+    d_ = np.searchsorted(np.array(K, dtype=np.uint64), k, side="left")
+    tie = np.zeros(n, dtype=bool)
+    inside = d_ < len(K)
+    tie[inside] = np.array(K, dtype=np.uint64)[d_[inside]] == k[inside]
+    cls = 2 * d_ + tie
+    cnt = np.bincount(cls, minlength=2 * G - 1)
+    start = np.concatenate([[0], np.cumsum(cnt)])
+    first = [next(i for i in range(G - 1) if K[i] == K[j]) for j in range(G - 1)]
+    cuts = [0]
+    for j in range(G - 1):
+        below = int((k < np.uint64(K[j])).sum())
+        cuts.append(int(start[2 * first[j] + 1]) + ((n * (j + 1)) // G - below))
+    cuts.append(n)
+    want = np.argsort(cls, kind="stable")
+    for fill in FILLS:
+        temp = temp_filled(tb, cuda, fill, seed=3)
+        tot = torch.empty(2 * G - 1, dtype=torch.int64, device=cuda)
+        _lib.check(L.fs_pair_classes_u64(kd.data_ptr(), n, Kd.data_ptr(), G, tot.data_ptr(), temp.data_ptr(), tb,
+                                         stream()), "classes")
+        np.testing.assert_array_equal(tot.cpu().numpy(), cnt)
+        dk = [Guarded(8 * (cuts[d + 1] - cuts[d]), cuda, 8 * d) for d in range(G)]
+        dv = [Guarded(4 * (cuts[d + 1] - cuts[d]), cuda, 4 * d) for d in range(G)]
+        c_ = (ctypes.c_uint64 * (G + 1))(*cuts)
+        b_ = (ctypes.c_uint64 * G)(*([0] * G))
+        pk = (ctypes.c_void_p * G)(*[g.ptr() for g in dk])
+        pv = (ctypes.c_void_p * G)(*[g.ptr() for g in dv])
+        _lib.check(L.fs_pair_scatter_u64_u32(kd.data_ptr(), vd.data_ptr(), n, Kd.data_ptr(), G, c_, b_, pk, pv,
+                                             temp.data_ptr(), tb, stream()), "scatter")
+        torch.cuda.synchronize()
+        for g in dk + dv:
+            assert g.guards_ok(), fill
+        for d in range(G):
+            sel = want[cuts[d]:cuts[d + 1]]
+            np.testing.assert_array_equal(dk[d].data(np.uint64), k[sel], err_msg=fill)
+            np.testing.assert_array_equal(dv[d].data(np.uint32), v[sel], err_msg=fill)
