@@ -53,7 +53,10 @@ __device__ unsigned long long g_expand_trace[1 << 16][4];
 namespace fs {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef FS_EXPAND_THREADS
+#define FS_EXPAND_THREADS 256
+#endif
+constexpr int kThreads = FS_EXPAND_THREADS;
 #ifndef FS_EXPAND_VPT
 #define FS_EXPAND_VPT 16
 #endif
@@ -139,7 +142,7 @@ FS_DEVINL void block_last_le2(const View& P, uint64_t nbins, uint64_t cs, uint64
 // the runtime value `vpt` (small outputs, smaller tiles).
 template <bool kTwoLevel, int kVpt>
 #ifndef FS_EXPAND_MINB
-#define FS_EXPAND_MINB 8  // CTAs per SM the register budget is sized for (32 registers)
+#define FS_EXPAND_MINB (2048 / FS_EXPAND_THREADS)  // CTAs per SM the register budget is sized for (32 registers)
 #endif
 __global__ void __launch_bounds__(kThreads, FS_EXPAND_MINB)
     k_expand16(const uint64_t* __restrict__ P, const uint64_t* __restrict__ slice_tot, uint64_t nbins, uint64_t pos0,
