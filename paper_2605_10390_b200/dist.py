@@ -310,7 +310,7 @@ def _exact_splitters(ops, level1_local, candidates, N: int, world: int, key_bits
 
 
 def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=None, key_bits: int = 64,
-                       mode: str = "P", peers=None):
+                       mode: str = "P", peers=None, events=None, stats=None):
     """Stable sort of the (u64 key, u32 value) pairs of all ranks (SURVEY.md §8(e)
     pairs, §8(f) NEXT-2): the ranks' shards are contiguous slices of the input in
     rank order, so the global stable order breaks key ties by (rank, local
@@ -328,6 +328,8 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
     mode "A" (payload all-to-all): stable local sort, cuts from the sorted shard,
     NCCL all_to_all of keys and values, stable local sort of what arrived.
     ``peers``: (keys, values) PeerBuffers to reuse across calls (mode "P").
+    ``events`` / ``stats``: as in sort_keys_u16 (around the payload exchange;
+    "sent_bytes" = 12 B per pair this rank sends to other ranks).
     """
     import numpy as np
     if keys.dtype != torch.uint64 or vals.dtype != torch.uint32 or keys.numel() != vals.numel():
@@ -374,7 +376,11 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
             peers = (PeerBuffers(dev, group, torch.uint64), PeerBuffers(dev, group, torch.uint32))
         cap = -(-N // world)
         pk, pv = peers[0].buffers(cap), peers[1].buffers(cap)
+        if stats is not None:
+            stats["sent_bytes"] = 12 * (n_local - (cuts[rank + 1] - cuts[rank]))
+        _mark(events, "x0")
         ex.scatter(cuts, bases, pk, pv)
+        _mark(events, "x1")
         ops.synchronize(dev)
         dist.barrier(group=group)                                   # every producer has finished writing
         rk, rv = pk[rank][:end - begin], pv[rank][:end - begin]
@@ -409,11 +415,15 @@ def sort_pairs_u64_u32(keys: torch.Tensor, vals: torch.Tensor, group=None, ops=N
         raise RuntimeError(f"mode A: rank {rank} receives {sum(recv)} pairs for a range of {end - begin}")
     rk = torch.empty(end - begin, dtype=torch.uint64, device=dev)
     rv = torch.empty(end - begin, dtype=torch.uint32, device=dev)
+    if stats is not None:
+        stats["sent_bytes"] = 12 * (n_local - send[rank])
     # NCCL / gloo have no unsigned 64/32-bit types: exchange the same bytes as int64 / int32
+    _mark(events, "x0")
     dist.all_to_all_single(rk.view(torch.int64), ks.view(torch.int64), output_split_sizes=recv,
                            input_split_sizes=send, group=group)
     dist.all_to_all_single(rv.view(torch.int32), vs.view(torch.int32), output_split_sizes=recv,
                            input_split_sizes=send, group=group)
+    _mark(events, "x1")
     if rk.numel():
         rk, rv = ops.sort_pairs(rk, rv)
     return (rk, rv), (begin, end)

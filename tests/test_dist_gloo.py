@@ -297,3 +297,63 @@ def test_distributed_pairs_match_oracle(tmp_path, world):
         ek, ev = oracle.sort_pairs_u64_u32(k, v)
         np.testing.assert_array_equal(np.concatenate(ks), ek, err_msg=f"{kind} {mode} world={world}")
         np.testing.assert_array_equal(np.concatenate(vs), ev, err_msg=f"{kind} {mode} world={world}")
+
+
+@pytest.mark.parametrize("G", [2, 3, 5, 8])
+@pytest.mark.parametrize("kind", ["uniform", "few", "const", "hi16"])
+def test_splitter_levels_and_cuts_single_process(G, kind):
+    """dist.splitter_level1 / splitter_refine / pair_cuts without collectives: the
+    per-rank histograms are summed here.  The splitters must be exactly the keys
+    at the rank boundaries of the stable global order, and every rank's cuts must
+    select exactly the elements the stable global sort gives each owner, in that
+    owner's order (lower rank first for ties)."""
+    import datagen
+    from paper_2605_10390_b200 import dist as fsd
+    n = 30_011
+    k = datagen.gen_u64(n, seed=G)
+    if kind == "few":
+        k = k % np.uint64(5)
+    elif kind == "const":
+        k = np.full(n, 77, dtype=np.uint64)
+    elif kind == "hi16":
+        k = (k & np.uint64((1 << 48) - 1)) | np.uint64(0xABCD << 48)
+    cuts_in = [0] + sorted(int(x) for x in datagen.gen_u64(G - 1, seed=1) % np.uint64(n)) + [n]
+    shards = [k[cuts_in[r]:cuts_in[r + 1]] for r in range(G)]
+    levels = fsd._levels(64)
+    bounds = [(n * d) // G for d in range(1, G)]
+    s1, w1 = levels[0]
+    H = sum(np.bincount((s >> np.uint64(s1)).astype(np.int64), minlength=1 << w1) for s in shards)
+    K, L = fsd.splitter_level1(H, bounds, s1)
+    for shift, width in levels[1:]:
+        Hl = np.zeros((G - 1, 1 << width), dtype=np.int64)
+        for s in shards:
+            hi = np.sort(s) >> np.uint64(shift)
+            for j, p in enumerate(K):
+                t = (np.uint64(p) >> np.uint64(shift)) | np.arange(1 << width, dtype=np.uint64)
+                Hl[j] += np.searchsorted(hi, t, side="right") - np.searchsorted(hi, t, side="left")
+        fsd.splitter_refine(Hl, bounds, K, L, shift)
+    order = np.argsort(k, kind="stable")                      # the stable global order
+    assert K == [int(k[order[b]]) for b in bounds]
+    assert L == [int((k < np.uint64(x)).sum()) for x in K]
+    # classes per rank, then every rank's cuts
+    Ka = np.array(K, dtype=np.uint64)
+    T_all = []
+    cls_all = []
+    for s in shards:
+        d = np.searchsorted(Ka, s, side="left")
+        tie = np.zeros(s.size, dtype=bool)
+        inside = d < Ka.size
+        tie[inside] = Ka[d[inside]] == s[inside]
+        c = 2 * d + tie
+        cls_all.append(c)
+        T_all.append(np.bincount(c, minlength=2 * G - 1))
+    cuts_all = fsd.pair_cuts(np.array(T_all), K, L, bounds, [s.size for s in shards])
+    owner_of = np.empty(n, dtype=np.int64)                   # global index -> owner, by the stable sort
+    for d in range(G):
+        owner_of[order[(n * d) // G:(n * (d + 1)) // G]] = d
+    for r, (s, c) in enumerate(zip(shards, cls_all)):
+        perm = np.argsort(c, kind="stable") + cuts_in[r]     # class order, as global indices
+        for d in range(G):
+            part = perm[cuts_all[r][d]:cuts_all[r][d + 1]]
+            assert np.all(owner_of[part] == d), (r, d)
+            assert part.size == int((owner_of[cuts_in[r]:cuts_in[r + 1]] == d).sum())
