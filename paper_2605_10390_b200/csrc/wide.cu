@@ -159,6 +159,9 @@ constexpr int kSegs = 256;              // first-level segments
 #ifndef FS_LOCAL_CB
 #define FS_LOCAL_CB 12
 #endif
+#ifndef FS_RANK_MASKED
+#define FS_RANK_MASKED 1
+#endif
 constexpr int kLocalThreads = FS_LOCAL_THREADS;
 constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in shared memory
 constexpr int kIdxBits = 14;            // local index bits of the composite key
@@ -1335,11 +1338,26 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
       heavy = 1;
       continue;
     }
+#if FS_RANK_MASKED
+    // branch-free: every key reads len entries from its group start and masks the
+    // ones past its group.  The reads stay inside the shared layout (s + len <= m
+    // + kMaxGroup, and perm, kCap u16, follows ck); an entry read past the group
+    // may be a perm slot another thread is writing -- its value is masked out.
+    static_assert(Cfg::kCap * 2 >= kMaxGroup * 8, "over-reads of ck stay inside perm");
+    uint32_t nu[kRankU];
+#pragma unroll
+    for (int u = 0; u < kRankU; ++u) nu[u] = e[u] - s[u];
+    for (uint32_t k = 0; k < len; ++k) {
+#pragma unroll
+      for (int u = 0; u < kRankU; ++u) r[u] += (uint32_t)((ck[s[u] + k] < c[u]) & (k < nu[u]));
+    }
+#else
     for (uint32_t k = 0; k < len; ++k) {
 #pragma unroll
       for (int u = 0; u < kRankU; ++u)
         if (s[u] + k < e[u]) r[u] += ck[s[u] + k] < c[u];
     }
+#endif
 #pragma unroll
     for (int u = 0; u < kRankU; ++u)
       if (j0 + u * kLocalThreads < m) fin[r[u]] = (uint16_t)(j0 + u * kLocalThreads);
