@@ -34,7 +34,8 @@
 //  * Runs of equal keys (sorted or constant inputs, ledger 21-22): a warp that
 //    sees an all-equal vector switches to an aggregating mode (one +8 per
 //    thread or one +256 per warp instead of same-address atomics); the check is
-//    sampled every 4th group while not aggregating.
+//    sampled every 4th group while not aggregating.  Vectors with mixed keys
+//    are queued per warp and counted 32 at a time by a full-warp add8.
 //  * Prologue zeroes the spill array (grid-strided) and the grid synchronises
 //    once, so the call needs no memset node.
 //  * Tail: each CTA flushes its partial (L2-resident), grid sync, then 128
@@ -181,7 +182,31 @@ FS_DEVINL bool all8_equal(const uint4& v) {
 // 334 us with ka alone; a warp-wide __reduce_add_sync of the run counts: constant
 // keys 192 -> 277 us.  profiles/r02/u16_variants_redirect.txt,
 // u16_variants_agg_redirect_lean.txt.)
-FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill) {
+#ifndef FS_HIST_MIXQ
+#define FS_HIST_MIXQ 1
+#endif
+// Per-warp queue of mixed vectors (FS_HIST_MIXQ): 64 uint4 slots in shared
+// memory after the dummy words, a ring read 32 at a time.
+constexpr int kMixQ = 64;
+struct MixQ {
+  uint4* q;      // this warp's ring
+  uint32_t h, n;  // head, entries (warp-uniform)
+};
+
+// Count the queued vectors [h, h + cnt) with one full-warp add8 (lane l takes slot h + l).
+FS_DEVINL void mixq_drain(uint32_t* sh, MixQ& mq, uint32_t cnt, unsigned long long* spill) {
+  __syncwarp();
+  const uint32_t lane = lane_id();
+  if (lane < cnt) {
+    const uint4 w = mq.q[(mq.h + lane) & (kMixQ - 1)];
+    if (add8(sh, w) & kHotMask) recheck8(sh, w, spill);
+  }
+  __syncwarp();  // the slots just read may be refilled by the next enqueue
+  mq.h = (mq.h + cnt) & (kMixQ - 1);
+  mq.n -= cnt;
+}
+
+FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill, MixQ& mq) {
   const uint32_t lane = lane_id();
   const bool eq = all8_equal(v);
   const uint32_t k0 = v.x & 0xFFFFu;
@@ -190,12 +215,30 @@ FS_DEVINL void add8_agg(uint32_t* sh, const uint4& v, unsigned long long* spill)
   const uint32_t mb = __ballot_sync(kFull, eq && k0 == kb && k0 != ka);
   if (lane == 0 && ma) add_key(sh, ka, 8u * __popc(ma), spill);
   if (lane == 31 && mb) add_key(sh, kb, 8u * __popc(mb), spill);
-  if (((ma | mb) >> lane) & 1u) return;
+  const bool in = ((ma | mb) >> lane) & 1u;
+#if FS_HIST_MIXQ
+  // A lane with mixed keys (a run boundary, or an outlier of a nearly sorted
+  // input: ~8% of c3c's vectors) is queued instead of issuing 8 atomics with
+  // the warp's other lanes idle; every 32 queued vectors are counted by one
+  // full-warp add8 (then checked, so the spill bound is unchanged: a thread
+  // adds at most 8 keys before its check).
+  if ((ma | mb) == kFull) return;  // warp-uniform: the whole warp is one or two runs (constant keys)
+  if (!in && eq) add_key(sh, k0, 8u, spill);
+  const bool mixed = !in && !eq;
+  const uint32_t mm = __ballot_sync(kFull, mixed);
+  if (mm) {  // warp-uniform
+    if (mixed) mq.q[(mq.h + mq.n + __popc(mm & lanemask_lt())) & (kMixQ - 1)] = v;
+    mq.n += __popc(mm);
+    if (mq.n >= 32) mixq_drain(sh, mq, 32, spill);
+  }
+#else
+  if (in) return;
   if (eq) {
     add_key(sh, k0, 8u, spill);
     return;
   }
   if (add8(sh, v) & kHotMask) recheck8(sh, v, spill);
+#endif
 }
 
 constexpr int kSliceBins = 512;                    // merge/scan granularity
@@ -266,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   uint32_t phase = 0;
   const uint32_t dummy_off = (kHistWords + tid) * 4u;  // this thread's dummy word (bank = lane, stays 0)
   uint32_t hot = 0xFFFFFFFFu, hot_cnt = 0;  // this warp's view of s_hot_key, refreshed every 4th group
+  MixQ mq{reinterpret_cast<uint4*>(sh + kHistWords + kThreads) + (tid >> 5) * kMixQ, 0u, 0u};
   // the whole warp calls this together (warp votes inside)
   auto process_v = [&](uint4 (&v)[kUnroll]) {
     if (agg || phase == 0) {
@@ -278,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     phase = (phase + 1) & 3;
     if (agg) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill);
+      for (int u = 0; u < kUnroll; ++u) add8_agg(sh, v[u], a.spill, mq);
     } else {
       uint32_t acc = 0;
       if (FS_HIST_HOT && (FS_HIST_HOT_ALWAYS || hot != 0xFFFFFFFFu)) {
@@ -339,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
       }
     }
   }
+  if (FS_HIST_MIXQ && mq.n) mixq_drain(sh, mq, mq.n, a.spill);  // the warp's last queued vectors
   if (FS_HIST_HOT && hot != 0xFFFFFFFFu) {  // keys counted in registers: added to the global spill once
     const uint32_t t = warp_sum(hot_cnt);
     if (lane_id() == 0 && t) atomicAdd(&a.spill[hot], (unsigned long long)t);
@@ -507,7 +552,8 @@ cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, 
                           uint64_t* slice_tot, int grid, cudaStream_t s) {
   static_assert(kHistWords % (4 * kThreads) == 0, "flush mapping");
   static_assert(kRowGroups * kSliceBins * 4 + 16 * 8 <= kHistWords * 4, "merge smem");
-  constexpr int smem = (kHistWords + kThreads) * 4;  // the table + one dummy word per thread
+  // the table + one dummy word per thread + the warps' mixed-vector queues
+  constexpr int smem = (kHistWords + kThreads) * 4 + (FS_HIST_MIXQ ? kThreads / 32 * kMixQ * 16 : 0);
   cudaError_t e = cudaFuncSetAttribute(k_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   HistArgs a;

@@ -1655,6 +1655,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 }
 
 #include "wide_heavy.cuh"
+#ifdef FS_LOCAL_PROBE
+float g_probe_ms[2];
+#endif
 
 // Bins of 2..kTinyMax keys, one warp each (a CTA's barriers and round trips
 // would cost more than the sort): every key's rank = #keys of the bin below it
@@ -2014,6 +2017,26 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
     if ((e = launch(k_heavy_items<K, kHasValues>, ((unsigned)(2 * sms)), kLocalThreads, lsmem, s, 
         kout, vout, alt_k, alt_v, hctl, (const HeavyItem*)(t + L.hitems), msd)) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+#ifdef FS_LOCAL_PROBE
+    // Debug probe (scripts/microbench variants only): re-sort the first
+    // FS_LOCAL_PROBE bins twice -- cold (evicted since the main launch) and warm
+    // (just written, L2-resident) -- and keep both durations.
+    if (sizeof(K) == 8 && kHasValues && !list_big) {
+      cudaEvent_t ev[3];
+      for (auto& x : ev) cudaEventCreate(&x);
+      cudaEventRecord(ev[0], s);
+      launch(k_local_sort<K, kHasValues>, (unsigned)FS_LOCAL_PROBE, kLocalThreads, lsmem, s, kout, vout, P16,
+             key_bits - kTopBits, msd, (const uint32_t*)nullptr, hctl);
+      cudaEventRecord(ev[1], s);
+      launch(k_local_sort<K, kHasValues>, (unsigned)FS_LOCAL_PROBE, kLocalThreads, lsmem, s, kout, vout, P16,
+             key_bits - kTopBits, msd, (const uint32_t*)nullptr, hctl);
+      cudaEventRecord(ev[2], s);
+      cudaEventSynchronize(ev[2]);
+      cudaEventElapsedTime(&g_probe_ms[0], ev[0], ev[1]);
+      cudaEventElapsedTime(&g_probe_ms[1], ev[1], ev[2]);
+      for (auto& x : ev) cudaEventDestroy(x);
+    }
+#endif
     phase_event(5, s);
   }
 
@@ -2062,3 +2085,7 @@ cudaError_t wide_sort(const void* keys_in, const uint32_t* vals_in, void* keys_o
 }
 
 }  // namespace fs
+
+#ifdef FS_LOCAL_PROBE
+extern "C" void fs_probe_local_ms(float* out) { out[0] = fs::g_probe_ms[0]; out[1] = fs::g_probe_ms[1]; }
+#endif

@@ -49,6 +49,23 @@ def test_sort_u16_all_equal(cuda, value):
     np.testing.assert_array_equal(out, keys)
 
 
+@pytest.mark.parametrize("nvals,swap", [(2, 0.01), (16, 0.02), (300, 0.05)])
+def test_sort_u16_nearly_sorted_spilling_runs(cuda, nvals, swap):
+    """Sorted runs long enough to spill (2^26 keys over a few values, every CTA's
+    run counters cross 2^15) with a fraction of random swaps: exercises the
+    aggregating path, its queue of mixed vectors (drained 32 at a time and at the
+    end of each warp's work) and the spill protocol together."""
+    n = (1 << 26) + 5
+    rng = np.random.default_rng(nvals)
+    vals = np.sort(rng.choice(65536, size=nvals, replace=False)).astype(np.uint16)
+    keys = np.repeat(vals, -(-n // nvals))[:n].copy()
+    i = rng.integers(0, n, size=int(n * swap))
+    j = rng.integers(0, n, size=i.size)
+    keys[i], keys[j] = keys[j], keys[i].copy()
+    out = to_host(fs.sort_keys(to_dev(keys, cuda)))
+    np.testing.assert_array_equal(out, oracle.sort_u16(keys))
+
+
 def test_sort_u16_two_hot_bins(cuda):
     """Adversarial for the 16-bit packed counters: both halves of one word are hot."""
     n = 1 << 23
