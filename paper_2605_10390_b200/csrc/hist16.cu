@@ -91,10 +91,20 @@ static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violate
 // The CTA's hot key (skewed inputs): the first key whose counter crossed 2^15
 // (0xFFFFFFFF: none yet).  Warps that see it count that key in registers.
 __shared__ uint32_t s_hot_key;
+// FS_HIST_HOT2W: a second hot word (the first spill of another word once the
+// first is set), redirected to a second per-thread dummy.
+#ifndef FS_HIST_HOT2W
+#define FS_HIST_HOT2W 1
+#endif
+__shared__ uint32_t s_hot_key2;
 
 FS_DEVINL void spill_word(uint32_t* sh, uint32_t w, unsigned long long* spill) {
   const uint32_t x = atomicExch(&sh[w], 0u);
-  if (FS_HIST_HOT) atomicCAS(&s_hot_key, 0xFFFFFFFFu, (x & 0xFFFFu) >= (x >> 16) ? 2 * w : 2 * w + 1);
+  if (FS_HIST_HOT) {
+    const uint32_t k = (x & 0xFFFFu) >= (x >> 16) ? 2 * w : 2 * w + 1;
+    const uint32_t prev = atomicCAS(&s_hot_key, 0xFFFFFFFFu, k);
+    if (FS_HIST_HOT2W && prev != 0xFFFFFFFFu && (prev >> 1) != w) atomicCAS(&s_hot_key2, 0xFFFFFFFFu, k);
+  }
   if (x & 0xFFFFu) atomicAdd(&spill[2 * w], (unsigned long long)(x & 0xFFFFu));
   if (x >> 16) atomicAdd(&spill[2 * w + 1], (unsigned long long)(x >> 16));
 }
@@ -132,14 +142,33 @@ FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
 #ifndef FS_HIST_REDIRECT
 #define FS_HIST_REDIRECT 1
 #endif
-FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc, uint32_t dummy_off) {
+// FS_HIST_HOTWORD: h is the hot key's word byte offset, the dummy counts both of
+// its keys (see below); folded into the spill by hot_dummy_flush.
+#ifndef FS_HIST_HOTWORD
+#define FS_HIST_HOTWORD 1
+#endif
+FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& hc, uint32_t dummy_off,
+                            uint32_t h2 = 0xFFFFFFFFu, uint32_t dummy2_off = 0) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   char* base = reinterpret_cast<char*>(sh);
   uint32_t acc = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t x = w[j];
-    if (FS_HIST_REDIRECT) {
+    if (FS_HIST_HOTWORD) {
+      // the hot key's whole counter WORD goes to the dummy with the normal
+      // increment: the dummy's halves count keys 2w and 2w + 1 exactly as the
+      // table's word would, so one word compare replaces key extraction,
+      // compare, increment select and register count.
+      const uint32_t a0 = (x + x) & 0x1FFFCu, a1 = (x >> 15) & 0x1FFFCu;
+      uint32_t b0 = a0 == h ? dummy_off : a0, b1 = a1 == h ? dummy_off : a1;
+      if (FS_HIST_HOT2W) {
+        b0 = a0 == h2 ? dummy2_off : b0;
+        b1 = a1 == h2 ? dummy2_off : b1;
+      }
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b0), (x & 1u) * 0xFFFFu + 1u);
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b1), max(x & 0x10000u, 1u));
+    } else if (FS_HIST_REDIRECT) {
       const bool pl = (x & 0xFFFFu) == h, ph = (x >> 16) == h;
       hc += (uint32_t)pl + (uint32_t)ph;
       acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + (pl ? dummy_off : ((x + x) & 0x1FFFCu))),
@@ -165,6 +194,19 @@ FS_DEVINL void recheck8(uint32_t* sh, const uint4& v, unsigned long long* spill)
     if (sh[a] & kHotMask) spill_word(sh, a, spill);
     if (sh[b] & kHotMask) spill_word(sh, b, spill);
   }
+}
+
+// FS_HIST_HOTWORD: move the dummy word's two halves (the hot word's keys 2w,
+// 2w + 1 counted by this thread) into the spill.  `force`: at the end; else only
+// once a half reached 2^15 (the dummy obeys the same bound as any table word).
+FS_DEVINL void hot_dummy_flush(uint32_t* sh, uint32_t dummy_off, uint32_t hot_key, unsigned long long* spill,
+                               bool force) {
+  uint32_t* d = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sh) + dummy_off);
+  if (!force && !(*d & kHotMask)) return;
+  const uint32_t x = atomicExch(d, 0u);
+  const uint32_t k0 = hot_key & ~1u;
+  if (x & 0xFFFFu) atomicAdd(&spill[k0], (unsigned long long)(x & 0xFFFFu));
+  if (x >> 16) atomicAdd(&spill[k0 + 1], (unsigned long long)(x >> 16));
 }
 
 FS_DEVINL bool all8_equal(const uint4& v) {
@@ -271,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   for (int i = 0; i < kHistWords / 4 / kThreads; ++i) smem_v4[tid + i * kThreads] = make_uint4(0, 0, 0, 0);
   sh[kHistWords + tid] = 0;  // dummy words (FS_HIST_REDIRECT)
   for (uint32_t i = blockIdx.x * kThreads + tid; i < kHistBins + 1; i += gridDim.x * kThreads) a.spill[i] = 0;
-  if (tid == 0) s_hot_key = 0xFFFFFFFFu;
+  if (tid == 0) s_hot_key = s_hot_key2 = 0xFFFFFFFFu;
+  if (FS_HIST_HOT2W) sh[kHistWords + kThreads + (FS_HIST_MIXQ ? kThreads / 32 * kMixQ * 4 : 0) + tid] = 0;
   grid.sync();
   FS_TRACE(1);
 
@@ -309,11 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   uint32_t phase = 0;
   const uint32_t dummy_off = (kHistWords + tid) * 4u;  // this thread's dummy word (bank = lane, stays 0)
   uint32_t hot = 0xFFFFFFFFu, hot_cnt = 0;  // this warp's view of s_hot_key, refreshed every 4th group
+  uint32_t hot2 = 0xFFFFFFFFu;
+  const uint32_t dummy2_off = (kHistWords + kThreads + (FS_HIST_MIXQ ? kThreads / 32 * kMixQ * 4 : 0) + tid) * 4u;
   MixQ mq{reinterpret_cast<uint4*>(sh + kHistWords + kThreads) + (tid >> 5) * kMixQ, 0u, 0u};
   // the whole warp calls this together (warp votes inside)
   auto process_v = [&](uint4 (&v)[kUnroll]) {
     if (agg || phase == 0) {
       if (FS_HIST_HOT) hot = s_hot_key;  // one broadcast load: warp-uniform
+      if (FS_HIST_HOT2W) hot2 = s_hot_key2;
       bool runs = false;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) runs |= all8_equal(v[u]);
@@ -327,7 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
       uint32_t acc = 0;
       if (FS_HIST_HOT && (FS_HIST_HOT_ALWAYS || hot != 0xFFFFFFFFu)) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) acc |= add8_hot(sh, v[u], hot, hot_cnt, dummy_off);
+        for (int u = 0; u < kUnroll; ++u)
+          acc |= add8_hot(sh, v[u], FS_HIST_HOTWORD ? (hot >> 1) * 4u : hot, hot_cnt, dummy_off, (hot2 >> 1) * 4u,
+                          dummy2_off);
+        if (FS_HIST_HOTWORD && (acc & kHotMask)) {
+          hot_dummy_flush(sh, dummy_off, hot, a.spill, false);
+          if (FS_HIST_HOT2W && hot2 != 0xFFFFFFFFu) hot_dummy_flush(sh, dummy2_off, hot2, a.spill, false);
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) acc |= add8(sh, v[u]);
@@ -384,7 +436,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
     }
   }
   if (FS_HIST_MIXQ && mq.n) mixq_drain(sh, mq, mq.n, a.spill);  // the warp's last queued vectors
-  if (FS_HIST_HOT && hot != 0xFFFFFFFFu) {  // keys counted in registers: added to the global spill once
+  if (FS_HIST_HOT && FS_HIST_HOTWORD && hot != 0xFFFFFFFFu) {
+    // this thread's dummy: the hot word's two counters -> warp sums -> the global spill once
+    const uint32_t x = sh[kHistWords + tid];
+    const uint32_t lo = warp_sum(x & 0xFFFFu), hi = warp_sum(x >> 16);
+    if (lane_id() == 0) {
+      if (lo) atomicAdd(&a.spill[hot & ~1u], (unsigned long long)lo);
+      if (hi) atomicAdd(&a.spill[hot | 1u], (unsigned long long)hi);
+    }
+  }
+  if (FS_HIST_HOT2W && hot2 != 0xFFFFFFFFu) {
+    const uint32_t x = sh[dummy2_off / 4];
+    const uint32_t lo = warp_sum(x & 0xFFFFu), hi = warp_sum(x >> 16);
+    if (lane_id() == 0) {
+      if (lo) atomicAdd(&a.spill[hot2 & ~1u], (unsigned long long)lo);
+      if (hi) atomicAdd(&a.spill[hot2 | 1u], (unsigned long long)hi);
+    }
+  }
+  if (FS_HIST_HOT && !FS_HIST_HOTWORD && hot != 0xFFFFFFFFu) {  // keys counted in registers: added to the global spill once
     const uint32_t t = warp_sum(hot_cnt);
     if (lane_id() == 0 && t) atomicAdd(&a.spill[hot], (unsigned long long)t);
   }
@@ -553,7 +622,8 @@ cudaError_t launch_hist16(const uint16_t* keys, uint64_t n, uint32_t* partials, 
   static_assert(kHistWords % (4 * kThreads) == 0, "flush mapping");
   static_assert(kRowGroups * kSliceBins * 4 + 16 * 8 <= kHistWords * 4, "merge smem");
   // the table + one dummy word per thread + the warps' mixed-vector queues
-  constexpr int smem = (kHistWords + kThreads) * 4 + (FS_HIST_MIXQ ? kThreads / 32 * kMixQ * 16 : 0);
+  constexpr int smem =
+      (kHistWords + kThreads) * 4 + (FS_HIST_MIXQ ? kThreads / 32 * kMixQ * 16 : 0) + (FS_HIST_HOT2W ? kThreads * 4 : 0);
   cudaError_t e = cudaFuncSetAttribute(k_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   HistArgs a;
