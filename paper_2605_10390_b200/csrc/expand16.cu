@@ -205,7 +205,18 @@ __global__ void __launch_bounds__(kThreads, FS_EXPAND_MINB)
   if (nvec == 0) return;
 
   const uint64_t tile_vec = (uint64_t)kThreads * vpt;  // vectors per tile (vpt <= kVecPerThread)
-  const uint64_t vec0 = (uint64_t)blockIdx.x * tile_vec;
+#ifndef FS_EXPAND_TILE_ORDER
+#define FS_EXPAND_TILE_ORDER 1
+#endif
+  // Tile order: CTAs b = 0, 1, 2, 3, ... take tiles 0, G-1, 1, G-2, ...  The
+  // slowest tiles of skewed inputs are the sparse ends of the key range (many
+  // short runs: Gauss tile 0 and G-1 take ~3x a dense tile, expand_trace.cu);
+  // dispatched first, they finish inside the first wave instead of extending
+  // the last one.  (Rotating only the last 16-256 tiles to the front instead:
+  // Gauss the same, Zipf 5 us slower -- profiles/r02/u16_variants_expand_order.txt.)
+  const uint64_t tile = FS_EXPAND_TILE_ORDER ? ((blockIdx.x & 1u) ? gridDim.x - 1u - (blockIdx.x >> 1) : (blockIdx.x >> 1))
+                                             : blockIdx.x;
+  const uint64_t vec0 = tile * tile_vec;
   const uint64_t vec_end = vec0 + tile_vec < nvec ? vec0 + tile_vec : nvec;
   const uint64_t o0 = pos0 + vec0 * 8;  // first global position of the tile
   const uint32_t len = (uint32_t)((vec_end - vec0) * 8);
@@ -288,20 +299,35 @@ __global__ void __launch_bounds__(kThreads, FS_EXPAND_MINB)
         const uint32_t pv = v | (v << 16);
         packed[0] = packed[1] = packed[2] = packed[3] = pv;
       } else {
+#ifndef FS_EXPAND_ONE_BOUNDARY
+#define FS_EXPAND_ONE_BOUNDARY 1
+#endif
         uint32_t jj = j;
+        const uint32_t je = FS_EXPAND_ONE_BOUNDARY ? advance(rel, j, hi, l + 7) : 0u;  // bin of the last key
+        if (FS_EXPAND_ONE_BOUNDARY && rel[je] == run_end) {
+          // one boundary (the bins between j and je are empty): keys before
+          // run_end are bin j, the rest bin je -- branch-free, so a warp whose
+          // lanes straddle runs of ~100 keys (Zipf) does not serialise on the
+          // per-key loop below
+          const uint32_t va = (uint32_t)(v_lo + j) & 0xFFFFu, vb = (uint32_t)(v_lo + je) & 0xFFFFu;
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          uint32_t pair = 0;
+          for (int e = 0; e < 8; e += 2)
+            packed[e / 2] = (l + e < run_end ? va : vb) | ((l + e + 1 < run_end ? va : vb) << 16);
+        } else {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t pos = l + e + h;
-            if (pos >= run_end) {
-              jj = advance(rel, jj, hi, pos);
-              run_end = rel[jj + 1];
+          for (int e = 0; e < 8; e += 2) {
+            uint32_t pair = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t pos = l + e + h;
+              if (pos >= run_end) {
+                jj = advance(rel, jj, hi, pos);
+                run_end = rel[jj + 1];
+              }
+              pair |= ((uint32_t)(v_lo + jj) & 0xFFFFu) << (16 * h);
             }
-            pair |= ((uint32_t)(v_lo + jj) & 0xFFFFu) << (16 * h);
+            packed[e / 2] = pair;
           }
-          packed[e / 2] = pair;
         }
       }
       st_stream_v4(dst + q, make_uint4(packed[0], packed[1], packed[2], packed[3]));

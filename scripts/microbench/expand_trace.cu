@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include "../../paper_2605_10390_b200/csrc/expand16.cu"
 
 namespace fs {
@@ -24,7 +26,29 @@ int main(int argc, char** argv) {
   const uint64_t n = argc > 1 ? strtoull(argv[1], 0, 0) : (1ull << 28);
   uint64_t *L, *tot; uint16_t* out;
   cudaMalloc(&L, 65536 * 8); cudaMalloc(&tot, 128 * 8); cudaMalloc(&out, n * 2);
-  mkprefix<<<256, 256>>>(L, tot, n / 65536);
+  const char* dist = argc > 2 ? argv[2] : "uniform";
+  if (!strcmp(dist, "uniform")) {
+    mkprefix<<<256, 256>>>(L, tot, n / 65536);
+  } else {  // gauss (mean 32768, sd 1024) or zipf (s = 1.2, values permuted): expected counts
+    std::vector<double> w(65536);
+    if (!strcmp(dist, "gauss")) {
+      for (int v = 0; v < 65536; ++v) w[v] = 0.5 * (erf((v + 0.5 - 32768) / 1024 / sqrt(2.0)) - erf((v - 0.5 - 32768) / 1024 / sqrt(2.0)));
+    } else {
+      std::vector<int> perm(65536);
+      for (int v = 0; v < 65536; ++v) perm[v] = v;
+      uint64_t x = 88172645463325252ull;
+      for (int v = 65535; v > 0; --v) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; std::swap(perm[v], perm[x % (v + 1)]); }
+      for (int r = 0; r < 65536; ++r) w[perm[r]] = pow(r + 1.0, -1.2);
+    }
+    double sw = 0; for (double y : w) sw += y;
+    std::vector<uint64_t> C(65536), hL(65536), ht(128, 0);
+    uint64_t tot_c = 0;
+    for (int v = 0; v < 65536; ++v) { C[v] = (uint64_t)(w[v] / sw * n); tot_c += C[v]; }
+    C[32768] += n - tot_c;
+    for (int s = 0; s < 128; ++s) { uint64_t run = 0; for (int j = 0; j < 512; ++j) { hL[s * 512 + j] = run; run += C[s * 512 + j]; } ht[s] = run; }
+    cudaMemcpy(L, hL.data(), 65536 * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(tot, ht.data(), 128 * 8, cudaMemcpyHostToDevice);
+  }
   cudaDeviceSynchronize();
   static unsigned long long tr[1 << 16][4];
   for (int rep = 0; rep < 4; ++rep) {
@@ -44,7 +68,13 @@ int main(int argc, char** argv) {
     printf("rep %d: event %.1f us, first start -> last end %.1f us, %d CTAs\n", rep, ms * 1e3, (tend - t0) / 1e3, G);
     printf("  setup us  p10 %.2f p50 %.2f p90 %.2f max %.2f\n", q(setup, .1), q(setup, .5), q(setup, .9), q(setup, 1));
     printf("  store us  p10 %.2f p50 %.2f p90 %.2f max %.2f\n", q(store, .1), q(store, .5), q(store, .9), q(store, 1));
-    if (rep == 3) {  // CTAs in setup / storing, per microsecond
+    if (rep == 3) {  // slowest CTAs, and CTAs in setup / storing per microsecond
+      std::vector<std::pair<double, int>> tot_t;
+      for (int c = 0; c < G; c++) tot_t.push_back({(tr[c][2] - tr[c][0]) / 1e3, c});
+      std::sort(tot_t.rbegin(), tot_t.rend());
+      printf("  slowest CTAs (us, tile):");
+      for (int i = 0; i < 12; ++i) printf(" %.1f@%d", tot_t[i].first, tot_t[i].second);
+      printf("\n");
       const int T = (int)((tend - t0) / 1000) + 1;
       std::vector<int> in_setup(T, 0), storing(T, 0);
       for (int c = 0; c < G; c++) {
