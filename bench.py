@@ -576,7 +576,10 @@ def run_fs(args, rank, world, local_rank):
                              "dram_bytes": traffic + t_exp,
                              "definition": "Eq. 1 (PAPER.md:432-436): useful / total DRAM bytes per sort; DRAM "
                                            "bytes = ncu dram__bytes_read.sum + dram__bytes_write.sum of hist16 and "
-                                           "expand16", "source": traffic_src}
+                                           "expand16", "source": traffic_src,
+                             "note": "above 1 when part of expand16's output is still dirty in the 126 MB L2 as "
+                                     "the kernel ends (write-back: ncu counts those writes in no launch); the "
+                                     "method moves no bytes beyond the useful ones at c2"}
 
     # End to end through the public host-buffer API: H2D of the step's keys from
     # pinned memory, the sort, D2H of the sorted keys, every step.
