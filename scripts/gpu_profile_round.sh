@@ -14,6 +14,8 @@ timeout 900 python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5.js
 timeout 900 python bench.py --workload c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c4_1gpu.json 2> $O/bench_c4.err
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_reference.json 2> $O/bench_reference.err
 rm -f scripts/microbench/variants/*.so
+# N>1 plumbing on the one GPU of the box (two ranks share it; gloo for the host collectives): every field of the N>1 line
+FS_BENCH_SHARE_GPU=1 FS_BENCH_BACKEND=gloo timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 > $O/bench_n2_shared.json 2> $O/bench_n2_shared.err; tail -c 600 $O/bench_n2_shared.json
 timeout 600 python scripts/microbench/wide_skew.py $((1 << 29)) > $O/wide_skew_c5size.txt 2>&1
 NB="--no-e2e --no-cpu-baseline --no-verify"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 5 --warmup 3 $NB > $O/ncu_launch_c2.log 2>&1
