@@ -1273,7 +1273,33 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
 
   FS_LPH(0);  // 0: key loads + composites + histogram atomics (+2 barriers)
   // ---- exclusive scan of the ngroups counters (thread t: words [t*wpt, (t+1)*wpt))
-  {
+#ifndef FS_LOCAL_VSCAN
+#define FS_LOCAL_VSCAN 1
+#endif
+  if (FS_LOCAL_VSCAN && nwords == 4u * kLocalThreads) {
+    // the common full-size case (4,096 groups, 512 threads; 2,048 / 256 for the
+    // mid bins): each thread's four words are one 16-byte shared load and store
+    // (four scalar loads at a 4-word stride were 4-way bank conflicts each)
+    uint4* cw4 = reinterpret_cast<uint4*>(cntw);
+    const uint4 x = cw4[tid];
+    const uint32_t a0 = (x.x & 0xFFFFu), a1 = (x.x >> 16), b0 = (x.y & 0xFFFFu), b1 = (x.y >> 16);
+    const uint32_t c0 = (x.z & 0xFFFFu), c1 = (x.z >> 16), d0 = (x.w & 0xFFFFu), d1 = (x.w >> 16);
+    const uint32_t local = a0 + a1 + b0 + b1 + c0 + c1 + d0 + d1;
+    const uint32_t inc = warp_inclusive_scan<uint32_t>(local);
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    uint32_t run = inc - local;
+    for (int w = 0; w < (int)warp; ++w) run += wtot[w];
+    uint4 y;
+    y.x = run | ((run + a0) << 16);
+    run += a0 + a1;
+    y.y = run | ((run + b0) << 16);
+    run += b0 + b1;
+    y.z = run | ((run + c0) << 16);
+    run += c0 + c1;
+    y.w = run | ((run + d0) << 16);
+    cw4[tid] = y;
+  } else {
     const uint32_t wpt = (nwords + kLocalThreads - 1) / kLocalThreads;  // <= 8
     const uint32_t w0 = tid * wpt;
     uint32_t local = 0;
