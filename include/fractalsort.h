@@ -19,7 +19,7 @@
  *    global memory of the current device), except where a name ends in _host.
  *    The caller owns every buffer; the library allocates no memory and keeps no
  *    state except a per-device attribute cache (thread-safe) and, for
- *    fs_sort_keys_u16_host only, one copy stream and 8 events per host thread
+ *    fs_sort_keys_u16_host only, two copy streams and 9 events per host thread
  *    and device, created on that thread's first call and kept for the process.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
  *    asynchronous and stream-ordered; there is no host synchronisation, so
@@ -288,10 +288,14 @@ fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_
  * serialises copies).  work: device workspace of
  * fs_sort_keys_u16_host_work_bytes(n, batch) bytes.  batch = 0 picks a default.
  * The call returns when the work is enqueued; synchronise `stream` before
- * reading keys_out_host.  The copies run on a copy stream of the library's
- * (one per host thread and device, created on first use and reused); if the
- * call fails after enqueuing work, `stream` is still made to wait for every
- * copy already queued, so later work on `stream` never races them.
+ * reading keys_out_host.  The copies run on two copy streams of the library's
+ * (host-to-device and device-to-host, one pair per host thread and device,
+ * created on first use and reused), so calls issued on DIFFERENT streams, each
+ * with its own work buffer and output, overlap one call's copy-out with the
+ * next call's copy-in (both PCIe directions busy); calls on one stream run in
+ * order.  If the call fails after enqueuing work, `stream` is still made to
+ * wait for every copy already queued, so later work on `stream` never races
+ * them.
  * ------------------------------------------------------------------------- */
 size_t fs_sort_keys_u16_host_work_bytes(uint64_t n, uint64_t batch);
 fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out_host, uint64_t n,

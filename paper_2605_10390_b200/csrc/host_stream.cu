@@ -6,8 +6,13 @@
 // batch is added into one reused histogram (fs_histogram_u16 accumulate = 1), so
 // batch switching costs no histogram rebuild.  After the last batch the scan
 // runs once and the output is reconstructed batch by batch (fs_expand_u16 over
-// output ranges) and streamed back.  Copies run on a private copy stream and
-// overlap the kernels of the neighbouring batch (double-buffered device slots).
+// output ranges) and streamed back.  Copies run on two private copy streams --
+// host->device on one, device->host on the other, so the two directions of the
+// PCIe link (two copy engines) can overlap -- and overlap the kernels of the
+// neighbouring batch (double-buffered device slots).  Within one call the
+// output cannot start before the last input batch is counted; calls issued on
+// different streams with their own work buffers overlap one call's output with
+// the next call's input.
 #include <cuda_runtime.h>
 
 #include "fractalsort.h"
@@ -51,15 +56,15 @@ HostLayout host_layout(uint64_t n, uint64_t batch) {
   return L;
 }
 
-// The copy stream and its 8 events, created on first use and kept for the life
-// of the process: one set per host thread and device (a thread's calls are
+// The copy streams (in: H2D, out: D2H) and 9 events, created on first use and
+// kept for the life of the process: one set per host thread and device (a thread's calls are
 // issued in order, so re-recording an event in a later call is safe -- a wait
 // captures the record current at the time of the wait; calls from other threads
 // use their own set).  No per-call stream or event creation.
 constexpr int kMaxDevices = 64;
 struct Resources {
-  cudaStream_t copy = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev[9] = {};
   bool ready = false;
 };
 thread_local Resources t_res[kMaxDevices];
@@ -71,8 +76,9 @@ cudaError_t resources(Resources*& R) {
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   R = &t_res[dev];
   if (R->ready) return cudaSuccess;
-  if (!R->copy && (e = cudaStreamCreateWithFlags(&R->copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
-  for (int i = 0; i < 8; ++i)
+  if (!R->copy_in && (e = cudaStreamCreateWithFlags(&R->copy_in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if (!R->copy_out && (e = cudaStreamCreateWithFlags(&R->copy_out, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  for (int i = 0; i < 9; ++i)
     if (!R->ev[i] && (e = cudaEventCreateWithFlags(&R->ev[i], cudaEventDisableTiming)) != cudaSuccess) return e;
   R->ready = true;
   return cudaSuccess;
@@ -108,27 +114,29 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
   cudaEvent_t* consumed = R->ev + 2; // [2] slot free again (hist or D2H done)
   cudaEvent_t* expanded = R->ev + 4; // [2]
   cudaEvent_t start = R->ev[6];
-  cudaEvent_t done = R->ev[7];
+  cudaEvent_t done_in = R->ev[7];
+  cudaEvent_t done_out = R->ev[8];
   // On an error after work was queued: order everything later on `stream` after
-  // the copies already queued on the copy stream (nothing is left dangling).
+  // the copies already queued on both copy streams (nothing is left dangling).
   auto drain = [&](fs_status st) {
-    if (cudaEventRecord(done, R->copy) == cudaSuccess) cudaStreamWaitEvent(s, done, 0);
+    if (cudaEventRecord(done_in, R->copy_in) == cudaSuccess) cudaStreamWaitEvent(s, done_in, 0);
+    if (cudaEventRecord(done_out, R->copy_out) == cudaSuccess) cudaStreamWaitEvent(s, done_out, 0);
     return st;
   };
 
-  // The copy stream starts after whatever the caller queued earlier on `stream`.
+  // The input copies start after whatever the caller queued earlier on `stream`.
   cudaEventRecord(start, s);
-  cudaStreamWaitEvent(R->copy, start, 0);
+  cudaStreamWaitEvent(R->copy_in, start, 0);
 
   const uint64_t B = L.batch, nb = (n + B - 1) / B;
   // ---- phase 1: stream batches in, one reused histogram
   for (uint64_t i = 0; i < nb; ++i) {
     const int slot = (int)(i & 1);
     const uint64_t len = (i + 1) * B <= n ? B : n - i * B;
-    if (i >= 2) cudaStreamWaitEvent(R->copy, consumed[slot], 0);
-    e = cudaMemcpyAsync(buf[slot], keys_in_host + i * B, len * 2, cudaMemcpyHostToDevice, R->copy);
+    if (i >= 2) cudaStreamWaitEvent(R->copy_in, consumed[slot], 0);
+    e = cudaMemcpyAsync(buf[slot], keys_in_host + i * B, len * 2, cudaMemcpyHostToDevice, R->copy_in);
     if (e != cudaSuccess) return drain(cuda_fail(e, "fs_sort_keys_u16_host: H2D"));
-    cudaEventRecord(copied[slot], R->copy);
+    cudaEventRecord(copied[slot], R->copy_in);
     cudaStreamWaitEvent(s, copied[slot], 0);
     fs_status st = fs_histogram_u16(buf[slot], len, 16, hist, i > 0, w + L.htemp, L.htemp_bytes, stream);
     if (st != FS_OK) return drain(st);
@@ -137,7 +145,8 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
   // ---- phase 2: one scan of the merged histogram
   fs_status st = fs_exclusive_scan_u64(hist, prefix, kHistBins, w + L.stemp, L.stemp_bytes, stream);
   if (st != FS_OK) return drain(st);
-  // ---- phase 3: reconstruct batch by batch and stream out
+  // ---- phase 3: reconstruct batch by batch and stream out (slots 0 and 1 were
+  //      last read by histograms on `stream`: stream order covers them)
   for (uint64_t j = 0; j < nb; ++j) {
     const int slot = (int)(j & 1);
     const uint64_t len = (j + 1) * B <= n ? B : n - j * B;
@@ -145,13 +154,13 @@ fs_status fs_sort_keys_u16_host(const uint16_t* keys_in_host, uint16_t* keys_out
     st = fs_expand_u16(prefix, kHistBins, j * B, j * B + len, buf[slot], stream);
     if (st != FS_OK) return drain(st);
     cudaEventRecord(expanded[slot], s);
-    cudaStreamWaitEvent(R->copy, expanded[slot], 0);
-    e = cudaMemcpyAsync(keys_out_host + j * B, buf[slot], len * 2, cudaMemcpyDeviceToHost, R->copy);
+    cudaStreamWaitEvent(R->copy_out, expanded[slot], 0);
+    e = cudaMemcpyAsync(keys_out_host + j * B, buf[slot], len * 2, cudaMemcpyDeviceToHost, R->copy_out);
     if (e != cudaSuccess) return drain(cuda_fail(e, "fs_sort_keys_u16_host: D2H"));
-    cudaEventRecord(consumed[slot], R->copy);
+    cudaEventRecord(consumed[slot], R->copy_out);
   }
-  cudaEventRecord(done, R->copy);
-  cudaStreamWaitEvent(s, done, 0);  // synchronising `stream` now implies the output is on the host
+  cudaEventRecord(done_out, R->copy_out);
+  cudaStreamWaitEvent(s, done_out, 0);  // synchronising `stream` now implies the output is on the host
   return finish(s, "fs_sort_keys_u16_host");
 }
 

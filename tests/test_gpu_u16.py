@@ -271,6 +271,32 @@ def test_host_streaming_sort(cuda):
     np.testing.assert_array_equal(out2.numpy(), oracle.sort_u16(keys))
 
 
+def test_host_streaming_sort_two_streams(cuda):
+    """Host-buffer sorts issued on two streams with their own work buffers
+    overlap (one call's copy-out with the other's copy-in, on the library's
+    separate H2D / D2H copy streams); a third call reuses stream A's work buffer
+    in stream order.  Every output must be the oracle's."""
+    n = (1 << 23) + 3
+    ka = datagen.gen_u16("uniform", n, seed=31)
+    kb = datagen.gen_u16("zipf", n, seed=32)
+    kc = datagen.gen_u16("sortedswap", n, seed=33)
+    srcs = [torch.from_numpy(k).pin_memory() for k in (ka, kb, kc)]
+    outs = [torch.empty(n, dtype=torch.uint16).pin_memory() for _ in range(3)]
+    need = fs.sort_keys_u16_host_work_bytes(n, 1 << 21)
+    wa = torch.empty(need, dtype=torch.uint8, device=cuda)
+    wb = torch.empty(need, dtype=torch.uint8, device=cuda)
+    sa, sb = torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)
+    with torch.cuda.stream(sa):
+        fs.sort_keys_u16_host(srcs[0], outs[0], batch=1 << 21, work=wa, synchronize=False)
+    with torch.cuda.stream(sb):
+        fs.sort_keys_u16_host(srcs[1], outs[1], batch=1 << 21, work=wb, synchronize=False)
+    with torch.cuda.stream(sa):
+        fs.sort_keys_u16_host(srcs[2], outs[2], batch=1 << 21, work=wa, synchronize=False)
+    torch.cuda.synchronize(cuda)
+    for k, o in zip((ka, kb, kc), outs):
+        np.testing.assert_array_equal(o.numpy(), oracle.sort_u16(k))
+
+
 def test_send_counts_matches_oracle(cuda):
     rng = np.random.default_rng(0)
     for G in [1, 2, 3, 8]:
