@@ -37,6 +37,21 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
+def _load_metrics():
+    """paper_2605_10390_b200/metrics.py by path: plain host arithmetic, without the
+    package's __init__ (which loads torch and the CUDA library the reference arm
+    does not need)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fs_metrics", os.path.join(ROOT, "paper_2605_10390_b200",
+                                                                            "metrics.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+metrics = _load_metrics()
+
 METRIC = "Gkeys/s and achieved HBM GB/s (% of roofline) at 1/2/4/8 B200"
 N_PER_GPU = 1 << 28
 C4_TOTAL = 1 << 34
@@ -166,9 +181,9 @@ def cpu_baseline_block(n: int, budget_s: float = 14.0):
         "value": round(vm / 1e9, 6), "unit": "Gkeys/s", "cores": nc, "kind": "oracle",
         "sample": (f"the full c2 input (2^28 keys), sorted {rm} times ({dm:.1f} s) by the oracle on {nc} threads "
                    f"(oracle_sort_u16_mt) and {r1} times ({d1:.1f} s) on one thread (oracle_sort_u16)"),
-        "T_unit_keys_per_s_per_core": round(vm / nc, 1),
+        "T_unit_keys_per_s_per_core": round(metrics.unit_throughput(n, n / vm, nc), 1),
         "single_thread": {"value": round(v1 / 1e9, 6), "unit": "Gkeys/s", "cores": 1,
-                          "T_unit_keys_per_s_per_core": round(v1, 1)},
+                          "T_unit_keys_per_s_per_core": round(metrics.unit_throughput(n, n / v1, 1), 1)},
         "host_GBps": round(4 * vm / 1e9, 2), "verified_nondecreasing": ok1 and okm,
         "cpu": cpu_model(), "host_cores": nc,
         "paper_context": "PAPER.md:417: 25.30e6 keys/s/core (i7-8665U, n_c = 4, 2^31 keys, 21.22 s)",
@@ -203,7 +218,7 @@ def run_reference(args, rank, world):
         "config": {"workload": WORKLOAD, "reference": "CPU oracle (oracle/oracle_mt.c: per-thread histograms, "
                                                       "merge, per-thread expansion), host cores"},
         "cpu_baseline": {"value": round(v, 6), "unit": "Gkeys/s", "cores": nc, "kind": "oracle", "sample": sample,
-                         "T_unit_keys_per_s_per_core": round(v * 1e9 / nc, 1),
+                         "T_unit_keys_per_s_per_core": round(metrics.unit_throughput(n * steps, dt, nc), 1),
                          "single_thread": {"value": round(v1 / 1e9, 6), "unit": "Gkeys/s", "cores": 1,
                                            "reps": r1, "seconds": round(d1, 2)},
                          "cpu": cpu_model(), "host_cores": nc},
@@ -417,7 +432,7 @@ def run_fs_pairs(args, dev):
     cand = [1, 2, 4] if path == "msd" else list(range(6, 14))
     dom = max(cand, key=lambda i: phase[i])
     peak, peak_src = measured_peak_gbs()
-    alg = 24 * n
+    alg = metrics.minimal_bytes_pairs(n, 8, 4)  # each MSD pass moves every pair once: read + write
     achieved = alg / (phase[dom] * 1e-3) / 1e9
     method_b = 80 * n if path == "msd" else 200 * n
     traffic, traffic_src = load_traffic(names[dom])
@@ -428,14 +443,15 @@ def run_fs_pairs(args, dev):
         "config": {"workload": "c5: 536,870,912 (u64 key uniform, u32 value = index) pairs, stable ascending sort",
                    "pairs": n, "l2": "inputs (6 GiB) larger than L2: no flush", "path": path},
         "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "unit": "GB/s", "frac": round(metrics.roofline_frac(alg, phase[dom] * 1e-3, peak), 4),
+                     "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(phase[dom], 4),
                      "peak_source": peak_src, "traffic_source": traffic_src,
                      "timing": f"phase events of a separate instrumented run of {isteps} sorts"},
-        "whole_step": {"minimal_bytes": 24 * n, "method_bytes": method_b,
-                       "frac_minimal_of_measured_peak": round(24 * n / (t_step * 1e-3) / 1e9 / peak, 4),
+        "whole_step": {"minimal_bytes": alg, "method_bytes": method_b,
+                       "frac_minimal_of_measured_peak": round(metrics.roofline_frac(alg, t_step * 1e-3, peak), 4),
                        "method_GBps": round(method_b / (t_step * 1e-3) / 1e9, 1),
-                       "frac_method_of_measured_peak": round(method_b / (t_step * 1e-3) / 1e9 / peak, 4)},
+                       "frac_method_of_measured_peak": round(metrics.roofline_frac(method_b, t_step * 1e-3, peak), 4)},
         "phases_ms": {nm: round(x, 4) for nm, x in zip(names, phase)},
         "ms_per_step_instrumented": round(inst_ms, 4),
         # MSD: 16 kernels (2 hist, window x2, scan, lists, plan, 2 vseg, 2 scatters, heavy,
@@ -541,7 +557,7 @@ def run_fs(args, rank, world, local_rank):
     peak, peak_src = measured_peak_gbs()
     achieved = alg_bytes / (names[dom] * 1e-3) / 1e9
     traffic, traffic_src = load_traffic(dom) if (args.workload == "c2" and world == 1) else (None, None)
-    whole_bytes = 4 * n
+    whole_bytes = metrics.minimal_bytes_keys(n, 2)  # the u16 sort reads and writes every key once
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step, 5), "higher_is_better": True,
@@ -554,13 +570,13 @@ def run_fs(args, rank, world, local_rank):
                    "l2": (f"inputs ({n * 2 / 2**20:.0f} MiB/GPU) larger than L2 (126 MB): no flush between steps"
                           if n * 2 > 126e6 else "L2-resident input (c1): launch-bound, no roofline claim")},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "frac": round(metrics.roofline_frac(alg_bytes, names[dom] * 1e-3, peak), 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(names[dom], 5),
                      "peak_source": peak_src, "traffic_source": traffic_src,
                      "timing": f"phase events of a separate instrumented run of {isteps} steps"},
         "whole_step": {"algorithmic_bytes": whole_bytes,
                        "achieved_GBps": round(whole_bytes / (t_step * 1e-3) / 1e9, 1),
-                       "frac_of_measured_peak": round(whole_bytes / (t_step * 1e-3) / 1e9 / peak, 4),
+                       "frac_of_measured_peak": round(metrics.roofline_frac(whole_bytes, t_step * 1e-3, peak), 4),
                        "frac_of_8TBps": round(whole_bytes / (t_step * 1e-3) / 8e12, 4)},
         "phases_ms": {k: round(v, 5) for k, v in zip(phase_names, phase_ms)},
         "ms_per_step_instrumented": round(inst_ms, 5),
@@ -572,7 +588,8 @@ def run_fs(args, rank, world, local_rank):
     if args.workload == "c2" and world == 1 and traffic is not None:
         t_exp, _ = load_traffic("expand16")
         if t_exp:
-            line["b_eff"] = {"value": round(whole_bytes / (traffic + t_exp), 4), "useful_bytes": whole_bytes,
+            line["b_eff"] = {"value": round(metrics.bandwidth_efficiency(whole_bytes, traffic + t_exp), 4),
+                             "useful_bytes": whole_bytes,
                              "dram_bytes": traffic + t_exp,
                              "definition": "Eq. 1 (PAPER.md:432-436): useful / total DRAM bytes per sort; DRAM "
                                            "bytes = ncu dram__bytes_read.sum + dram__bytes_write.sum of hist16 and "
