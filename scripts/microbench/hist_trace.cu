@@ -4,6 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DFS_HIST_TRACE \
 //        -I../../include -I../../paper_2605_10390_b200/csrc -o ht hist_trace.cu
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <algorithm>
 #include "../../paper_2605_10390_b200/csrc/hist16.cu"
@@ -14,9 +15,9 @@ const DeviceInfo& device_info() { static DeviceInfo d; if (!d.sm_count) cudaDevi
 __device__ __forceinline__ uint64_t sm64(uint64_t z){z+=0x9E3779B97F4A7C15ull;z=(z^(z>>30))*0xBF58476D1CE4E5B9ull;z=(z^(z>>27))*0x94D049BB133111EBull;return z^(z>>31);}
 __global__ void gen(uint16_t* k, uint64_t n){ for(uint64_t i=blockIdx.x*(uint64_t)blockDim.x+threadIdx.x;i<n;i+=(uint64_t)gridDim.x*blockDim.x) k[i]=(uint16_t)(sm64(i)>>48); }
 
-int main(){
+int main(int argc, char** argv){
   setvbuf(stdout,NULL,_IONBF,0);
-  uint64_t n=1ull<<28; uint16_t* k; uint32_t* part; unsigned long long *sp; uint64_t *st; uint32_t* rw; uint64_t* P;
+  uint64_t n=argc>1?strtoull(argv[1],nullptr,0):1ull<<28; uint16_t* k; uint32_t* part; unsigned long long *sp; uint64_t *st; uint32_t* rw; uint64_t* P;
   int G=fs::hist16_grid(n);
   cudaMalloc(&k,n*2); cudaMalloc(&part,(size_t)G*131072); cudaMalloc(&sp,(65536+32)*8); cudaMalloc(&st,129*8); cudaMalloc(&rw,1024); cudaMalloc(&P,65537*8);
   gen<<<1184,256>>>(k,n); cudaDeviceSynchronize();
