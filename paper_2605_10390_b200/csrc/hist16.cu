@@ -606,9 +606,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
 
 int hist16_grid(uint64_t n) {
 #ifndef FS_HIST_KEYS_PER_CTA
-#define FS_HIST_KEYS_PER_CTA 65536
+#define FS_HIST_KEYS_PER_CTA 8192
 #endif
-  // keep >= FS_HIST_KEYS_PER_CTA keys per CTA: every CTA zeroes and flushes 128 KB
+  // keep >= FS_HIST_KEYS_PER_CTA keys per CTA: every CTA zeroes and flushes 128 KB,
+  // but below ~2^24 keys the loop is short and more CTAs win (u16 sort b2b,
+  // 65,536 -> 8,192 keys per CTA: 2^20 26.8 -> 23.0 us, 2^22 33.0 -> 29.1 us,
+  // 2^24 unchanged; profiles/r02d/u16_variants_keys_per_cta.txt)
   const uint64_t want = (n + FS_HIST_KEYS_PER_CTA - 1) / FS_HIST_KEYS_PER_CTA;
   const uint64_t sms = (uint64_t)device_info().sm_count;
   uint64_t g = want < sms ? want : sms;
