@@ -285,6 +285,8 @@ def timed(step, steps: int, warmup: int, dev, dist, clocks_index=None):
         for _ in range(steps):
             step()
         b.record(stream)
+        while not b.query():  # wait without holding the GIL, so the clock sampler thread runs
+            time.sleep(0.0001)
         torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
