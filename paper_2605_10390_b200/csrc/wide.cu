@@ -1923,6 +1923,12 @@ cudaError_t run(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, uint
   sa.tma = tma ? 1 : 0;
 
   phase_event(0, s);
+  // The lookback status words (the bulk of this range: (tiles + tiles/4 + 512) x 2 KB,
+  // ~50 us at c5) are zeroed on every call.  Their pass tags keep the passes of one
+  // call apart, but the caller's temp may hold anything (the memory-safety tests fill
+  // it with random bytes), and a stale or random word carrying the right tag and a
+  // set flag would be read as a published prefix; no tag or epoch width makes that
+  // impossible, so the zeroing stays.
   if ((e = cudaMemsetAsync(t + L.zero_begin, 0, L.zero_end - L.zero_begin, s)) != cudaSuccess) return e;
 
   if (L.use_msd) {
