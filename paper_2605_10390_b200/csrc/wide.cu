@@ -167,7 +167,10 @@ constexpr int kLocalCap = 8704;         // max keys of a 16-bit bin sorted in sh
 constexpr int kIdxBits = 14;            // local index bits of the composite key
 static_assert(kLocalCap <= (1 << kIdxBits), "local index must fit");
 constexpr int kCountBitsMax = FS_LOCAL_CB;  // local counting digit (<= 4,096 groups)
-constexpr int kRankU = 4;              // keys ranked at once per thread (ILP)
+#ifndef FS_RANK_U
+#define FS_RANK_U 4
+#endif
+constexpr int kRankU = FS_RANK_U;       // keys ranked at once per thread (ILP)
 constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
 #ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
 #define FS_TINY_MAX 128
