@@ -171,7 +171,20 @@ constexpr int kCountBitsMax = FS_LOCAL_CB;  // local counting digit (<= 4,096 gr
 #define FS_RANK_U 4
 #endif
 constexpr int kRankU = FS_RANK_U;       // keys ranked at once per thread (ILP)
-constexpr int kMaxGroup = 32;           // insertion-sort bound of the fast path
+// Fast path or slow path, per bin, from the counting digit's group sizes L_g:
+// the rank loop costs ~ L per key (sum L_g^2 over the bin), the slow path's LSD a
+// fixed ~6 multisplit passes; a bin takes the slow path if some group exceeds
+// kMaxGroup or the key-weighted mean group size sum(L_g^2) / m exceeds
+// kMeanGroupMax (repeated keys: 16 copies of each key, 2^29 pairs: local sort
+// 25.5 -> 7.3 ms; 64 copies stay on the slow path; profiles/r02d/wide_skew_dup.txt).
+#ifndef FS_MAX_GROUP
+#define FS_MAX_GROUP 128
+#endif
+#ifndef FS_MEAN_GROUP
+#define FS_MEAN_GROUP 48
+#endif
+constexpr int kMaxGroup = FS_MAX_GROUP;  // rank-loop bound of the fast path
+constexpr int kMeanGroupMax = FS_MEAN_GROUP;
 #ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
 #define FS_TINY_MAX 128
 #endif
@@ -1238,7 +1251,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm);
   uint32_t* cntw = reinterpret_cast<uint32_t*>(smem_raw + Lay::scratch);
   uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cntw);
-  __shared__ uint32_t heavy;
+  __shared__ uint32_t heavy, s_sq, s_maxl;
   __shared__ uint32_t wtot[kLocalWarps];
   __shared__ unsigned long long or_all, and_all;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -1250,7 +1263,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   const uint32_t nwords = (ngroups + 1) >> 1;
   const int cshift = kIdxBits + R - cb;
 
-  if (tid == 0) heavy = 0;
+  if (tid == 0) heavy = s_sq = s_maxl = 0;
   // Keys: all loads in flight at once, turned into composites that stay in
   // registers; the digit histogram is counted from them; after the scan each
   // composite is written straight to its group's slot (ck is filled in group
@@ -1288,6 +1301,13 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
     const uint32_t a0 = (x.x & 0xFFFFu), a1 = (x.x >> 16), b0 = (x.y & 0xFFFFu), b1 = (x.y >> 16);
     const uint32_t c0 = (x.z & 0xFFFFu), c1 = (x.z >> 16), d0 = (x.w & 0xFFFFu), d1 = (x.w >> 16);
     const uint32_t local = a0 + a1 + b0 + b1 + c0 + c1 + d0 + d1;
+    const uint32_t sq = a0 * a0 + a1 * a1 + b0 * b0 + b1 * b1 + c0 * c0 + c1 * c1 + d0 * d0 + d1 * d1;
+    const uint32_t mx = max(max(max(a0, a1), max(b0, b1)), max(max(c0, c1), max(d0, d1)));
+    const uint32_t wsq = __reduce_add_sync(kFull, sq), wmx = __reduce_max_sync(kFull, mx);
+    if (lane == 0) {
+      atomicAdd(&s_sq, wsq);
+      atomicMax(&s_maxl, wmx);
+    }
     const uint32_t inc = warp_inclusive_scan<uint32_t>(local);
     if (lane == 31) wtot[warp] = inc;
     __syncthreads();
@@ -1305,12 +1325,19 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   } else {
     const uint32_t wpt = (nwords + kLocalThreads - 1) / kLocalThreads;  // <= 8
     const uint32_t w0 = tid * wpt;
-    uint32_t local = 0;
+    uint32_t local = 0, sq = 0, mx = 0;
     for (uint32_t j = 0; j < wpt; ++j)
       if (w0 + j < nwords) {
-        const uint32_t x = cntw[w0 + j];
-        local += (x & 0xFFFFu) + (x >> 16);
+        const uint32_t x = cntw[w0 + j], lo = x & 0xFFFFu, hi = x >> 16;
+        local += lo + hi;
+        sq += lo * lo + hi * hi;
+        mx = max(mx, max(lo, hi));
       }
+    const uint32_t wsq = __reduce_add_sync(kFull, sq), wmx = __reduce_max_sync(kFull, mx);
+    if (lane == 0) {
+      atomicAdd(&s_sq, wsq);
+      atomicMax(&s_maxl, wmx);
+    }
     const uint32_t inc = warp_inclusive_scan<uint32_t>(local);
     if (lane == 31) wtot[warp] = inc;
     __syncthreads();
@@ -1325,6 +1352,8 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
       }
   }
   __syncthreads();
+  // (read by every thread after the counting scatter's barrier)
+  if (tid == 0 && (s_maxl > (uint32_t)kMaxGroup || s_sq > (uint32_t)kMeanGroupMax * m)) heavy = 1;
 
   FS_LPH(1);  // 1: scan
   // ---- counting scatter of the composites (order inside a group is fixed below)
@@ -1349,7 +1378,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   // (Measured at c5: 4.41 ms vs 4.50 for one key at a time with the keys
   // stored from here, 4.74 for one at a time staged, 5.34 for kRankU = 8; an
   // insertion sort per group, one thread per group: 5.15.)
-  for (uint32_t j0 = tid; j0 < m; j0 += kRankU * kLocalThreads) {
+  for (uint32_t j0 = heavy ? m : tid; j0 < m; j0 += kRankU * kLocalThreads) {  // slow-path bins skip the ranks
     uint64_t c[kRankU];
     uint32_t s[kRankU], e[kRankU], r[kRankU];
     uint32_t len = 0;
@@ -1363,10 +1392,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
       r[u] = s[u];
       len = max(len, e[u] - s[u]);
     }
-    if (len > (uint32_t)kMaxGroup) {  // a group > kMaxGroup: the whole bin takes the slow path
-      heavy = 1;
-      continue;
-    }
+    if (len > (uint32_t)kMaxGroup) continue;  // never: such a bin was sent to the slow path above
 #if FS_RANK_MASKED
     // branch-free: every key reads len entries from its group start and masks the
     // ones past its group.  The reads stay inside the shared layout (s + len <= m

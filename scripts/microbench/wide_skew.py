@@ -33,6 +33,9 @@ def make(kind):
     elif kind.startswith("lt2^"):  # a common zero prefix: keys < 2^b
         b = int(kind[4:])
         ki[:] = ki & ((1 << b) - 1)
+    elif kind.startswith("dup"):  # every key repeated ~m times: m = 8 -> "dup8" (2^29 / 8 distinct values)
+        m = int(kind[3:])
+        ki[:] = ki[ri & (n // m - 1)]
     elif kind == "clustered":  # 64 clusters, each 2^-8 wide in the key space (about 256 bins each)
         c = (ri & 63) * 0x0400_0000_0000_0000 // 1
         ki[:] = (c + (ki & ((1 << 56) - 1)))
