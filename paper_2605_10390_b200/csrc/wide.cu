@@ -185,6 +185,20 @@ constexpr int kRankU = FS_RANK_U;       // keys ranked at once per thread (ILP)
 #endif
 constexpr int kMaxGroup = FS_MAX_GROUP;  // rank-loop bound of the fast path
 constexpr int kMeanGroupMax = FS_MEAN_GROUP;
+// Bins that fail that test but whose groups all hold <= kWarpSortMax keys sort
+// every group in place with one warp's bitonic network (registers and shuffles:
+// composites are read and written once) instead of the slow path's six
+// permutation passes (FS_WARP_SORT_MAX = 0: off).
+#ifndef FS_WARP_SORT_MAX
+#define FS_WARP_SORT_MAX 256
+#endif
+constexpr int kWarpSortMax = FS_WARP_SORT_MAX;
+#ifndef FS_WARP_SORT_MEAN  // ... and key-weighted mean group size <= this (N log^2 N networks lose to the
+#define FS_WARP_SORT_MEAN 96  // passes beyond it)
+#endif
+constexpr int kWarpSortMean = FS_WARP_SORT_MEAN;
+static_assert(kWarpSortMax == 0 || kWarpSortMax == 32 || kWarpSortMax == 64 || kWarpSortMax == 128 ||
+                  kWarpSortMax == 256, "warp sort sizes");
 #ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
 #define FS_TINY_MAX 128
 #endif
@@ -307,6 +321,56 @@ FS_DEVINL uint32_t match_digit8(uint32_t d, uint32_t valid) {
         : "r"(d), "r"(1u << b));
   }
   return peers;
+}
+
+// Ascending bitonic sort of 32 * P 64-bit values held by one warp (element
+// p * 32 + lane in x[p]); partners closer than 32 are exchanged by shuffles,
+// farther ones inside the lane's registers.  Every loop is unrolled at compile
+// time.  (Used by the per-bin sort for groups of repeated keys.)
+template <int P>
+FS_DEVINL void warp_bitonic_sort(uint64_t (&x)[P]) {
+  const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int k = 2; k <= 32 * P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const bool up = (((uint32_t)p * 32u + lane) & (uint32_t)k) == 0;
+        if (j >= 32) {
+          const int q = p ^ (j / 32);
+          if (q > p) {
+            const uint64_t a = x[p], b = x[q];
+            const bool sw = up ? (a > b) : (a < b);
+            x[p] = sw ? b : a;
+            x[q] = sw ? a : b;
+          }
+        } else {
+          const uint64_t y = __shfl_xor_sync(kFull, x[p], j);
+          const bool keep_min = ((lane & (uint32_t)j) == 0) == up;
+          x[p] = keep_min ? (y < x[p] ? y : x[p]) : (y > x[p] ? y : x[p]);
+        }
+      }
+    }
+  }
+}
+
+// Sort ck[s, s + L) in place (one warp, L <= 32 * P); padding sorts last.
+template <int P>
+FS_DEVINL void warp_sort_group(uint64_t* ck, uint32_t s, uint32_t L) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t x[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint32_t i = (uint32_t)p * 32u + lane;
+    x[p] = i < L ? ck[s + i] : ~0ull;
+  }
+  warp_bitonic_sort<P>(x);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint32_t i = (uint32_t)p * 32u + lane;
+    if (i < L) ck[s + i] = x[p];
+  }
 }
 
 template <typename K>
@@ -1353,7 +1417,9 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   }
   __syncthreads();
   // (read by every thread after the counting scatter's barrier)
-  if (tid == 0 && (s_maxl > (uint32_t)kMaxGroup || s_sq > (uint32_t)kMeanGroupMax * m)) heavy = 1;
+  // path: 0 rank loop, 1 per-group warp sorts, 2 slow path (heavy)
+  if (tid == 0 && (s_maxl > (uint32_t)kMaxGroup || s_sq > (uint32_t)kMeanGroupMax * m))
+    heavy = (s_maxl <= (uint32_t)kWarpSortMax && s_sq <= (uint32_t)kWarpSortMean * m) ? 1u : 2u;
 
   FS_LPH(1);  // 1: scan
   // ---- counting scatter of the composites (order inside a group is fixed below)
@@ -1421,7 +1487,18 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
 
   FS_LPH(3);  // 3: ranks
   uint16_t* pfinal = fin;
-  if (heavy) {
+  const bool in_place = heavy == 1;  // the groups are sorted where they lie: position j holds slot j
+  if (in_place) {
+    for (uint32_t g = warp; g < ngroups; g += kLocalWarps) {
+      const uint32_t gs = g ? cnt16[g - 1] : 0u, L = (uint32_t)cnt16[g] - gs;
+      if (L <= 1) continue;
+      if (kWarpSortMax >= 32 && L <= 32) warp_sort_group<1>(ck, gs, L);
+      else if (kWarpSortMax >= 64 && L <= 64) warp_sort_group<2>(ck, gs, L);
+      else if (kWarpSortMax >= 128 && L <= 128) warp_sort_group<4>(ck, gs, L);
+      else if (kWarpSortMax >= 256) warp_sort_group<8>(ck, gs, L);
+    }
+    __syncthreads();
+  } else if (heavy) {
     // ---- slow path: stable LSD over the varying 8-bit digits of the R bits
     uint16_t* pa = perm;
     uint16_t* pb = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm_b);
@@ -1511,7 +1588,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   {
 #pragma unroll 4
     for (uint32_t j = tid; j < m; j += kLocalThreads) {
-      const uint64_t c = ck[pfinal[j]];
+      const uint64_t c = ck[in_place ? j : pfinal[j]];
       kout[b0 + j] = top + (K)(c >> kIdxBits);
       pfinal[j] = (uint16_t)(c & ((1u << kIdxBits) - 1));
     }

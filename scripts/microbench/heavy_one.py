@@ -20,6 +20,8 @@ if kind == "hot1x50":
     ki[:] = torch.where((ri & 1) == 0, (0x7777 << 48) | low48, ki)
 elif kind == "hot16x25":
     ki[:] = torch.where((ri & 3) == 0, ((((ri >> 8) & 15) * 0x0F0F + 0x1234) << 48) | low48, ki)
+elif kind.startswith("dup"):  # every key repeated ~M times ("dup64")
+    ki[:] = ki[ri & (n // int(kind[3:]) - 1)]
 elif kind == "clustered":
     ki[:] = (ri & 63) * 0x0400_0000_0000_0000 + (ki & ((1 << 56) - 1))
 v = torch.arange(n, dtype=torch.int32, device=dev).view(torch.uint32)
