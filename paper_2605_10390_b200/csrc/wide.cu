@@ -172,11 +172,13 @@ constexpr int kCountBitsMax = FS_LOCAL_CB;  // local counting digit (<= 4,096 gr
 #endif
 constexpr int kRankU = FS_RANK_U;       // keys ranked at once per thread (ILP)
 // Fast path or slow path, per bin, from the counting digit's group sizes L_g:
-// the rank loop costs ~ L per key (sum L_g^2 over the bin), the slow path's LSD a
-// fixed ~6 multisplit passes; a bin takes the slow path if some group exceeds
+// the rank loop costs ~ L per key (sum L_g^2 over the bin), the slow path a fixed
+// number of multisplit passes; a bin takes the slow path if some group exceeds
 // kMaxGroup or the key-weighted mean group size sum(L_g^2) / m exceeds
-// kMeanGroupMax (repeated keys: 16 copies of each key, 2^29 pairs: local sort
-// 25.5 -> 7.3 ms; 64 copies stay on the slow path; profiles/r02d/wide_skew_dup.txt).
+// kMeanGroupMax (repeated keys, 2^29 pairs, 16 copies of each key: local sort
+// 25.5 -> 7.3 ms; profiles/r02d/wide_skew_dup.txt).  The slow path sorts by the
+// counting digit first (two stable passes) and finishes groups of <=
+// kGroupValuesMax distinct keys by value sweeps, else runs the full LSD.
 #ifndef FS_MAX_GROUP
 #define FS_MAX_GROUP 128
 #endif
@@ -185,20 +187,10 @@ constexpr int kRankU = FS_RANK_U;       // keys ranked at once per thread (ILP)
 #endif
 constexpr int kMaxGroup = FS_MAX_GROUP;  // rank-loop bound of the fast path
 constexpr int kMeanGroupMax = FS_MEAN_GROUP;
-// Bins that fail that test but whose groups all hold <= kWarpSortMax keys sort
-// every group in place with one warp's bitonic network (registers and shuffles:
-// composites are read and written once) instead of the slow path's six
-// permutation passes (FS_WARP_SORT_MAX = 0: off).
-#ifndef FS_WARP_SORT_MAX
-#define FS_WARP_SORT_MAX 256
+#ifndef FS_GROUP_VALUES_MAX  // slow path: most distinct keys in one group sorted by value sweeps (else the full LSD)
+#define FS_GROUP_VALUES_MAX 16
 #endif
-constexpr int kWarpSortMax = FS_WARP_SORT_MAX;
-#ifndef FS_WARP_SORT_MEAN  // ... and key-weighted mean group size <= this (N log^2 N networks lose to the
-#define FS_WARP_SORT_MEAN 96  // passes beyond it)
-#endif
-constexpr int kWarpSortMean = FS_WARP_SORT_MEAN;
-static_assert(kWarpSortMax == 0 || kWarpSortMax == 32 || kWarpSortMax == 64 || kWarpSortMax == 128 ||
-                  kWarpSortMax == 256, "warp sort sizes");
+constexpr int kGroupValuesMax = FS_GROUP_VALUES_MAX;
 #ifndef FS_TINY_MAX  // bins of <= this many keys: one warp each (multiple of 32)
 #define FS_TINY_MAX 128
 #endif
@@ -321,56 +313,6 @@ FS_DEVINL uint32_t match_digit8(uint32_t d, uint32_t valid) {
         : "r"(d), "r"(1u << b));
   }
   return peers;
-}
-
-// Ascending bitonic sort of 32 * P 64-bit values held by one warp (element
-// p * 32 + lane in x[p]); partners closer than 32 are exchanged by shuffles,
-// farther ones inside the lane's registers.  Every loop is unrolled at compile
-// time.  (Used by the per-bin sort for groups of repeated keys.)
-template <int P>
-FS_DEVINL void warp_bitonic_sort(uint64_t (&x)[P]) {
-  const uint32_t lane = threadIdx.x & 31u;
-#pragma unroll
-  for (int k = 2; k <= 32 * P; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const bool up = (((uint32_t)p * 32u + lane) & (uint32_t)k) == 0;
-        if (j >= 32) {
-          const int q = p ^ (j / 32);
-          if (q > p) {
-            const uint64_t a = x[p], b = x[q];
-            const bool sw = up ? (a > b) : (a < b);
-            x[p] = sw ? b : a;
-            x[q] = sw ? a : b;
-          }
-        } else {
-          const uint64_t y = __shfl_xor_sync(kFull, x[p], j);
-          const bool keep_min = ((lane & (uint32_t)j) == 0) == up;
-          x[p] = keep_min ? (y < x[p] ? y : x[p]) : (y > x[p] ? y : x[p]);
-        }
-      }
-    }
-  }
-}
-
-// Sort ck[s, s + L) in place (one warp, L <= 32 * P); padding sorts last.
-template <int P>
-FS_DEVINL void warp_sort_group(uint64_t* ck, uint32_t s, uint32_t L) {
-  const uint32_t lane = threadIdx.x & 31u;
-  uint64_t x[P];
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const uint32_t i = (uint32_t)p * 32u + lane;
-    x[p] = i < L ? ck[s + i] : ~0ull;
-  }
-  warp_bitonic_sort<P>(x);
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const uint32_t i = (uint32_t)p * 32u + lane;
-    if (i < L) ck[s + i] = x[p];
-  }
 }
 
 template <typename K>
@@ -1315,7 +1257,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm);
   uint32_t* cntw = reinterpret_cast<uint32_t*>(smem_raw + Lay::scratch);
   uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cntw);
-  __shared__ uint32_t heavy, s_sq, s_maxl;
+  __shared__ uint32_t heavy, s_sq, s_maxl, s_fallback;
   __shared__ uint32_t wtot[kLocalWarps];
   __shared__ unsigned long long or_all, and_all;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -1417,9 +1359,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   }
   __syncthreads();
   // (read by every thread after the counting scatter's barrier)
-  // path: 0 rank loop, 1 per-group warp sorts, 2 slow path (heavy)
-  if (tid == 0 && (s_maxl > (uint32_t)kMaxGroup || s_sq > (uint32_t)kMeanGroupMax * m))
-    heavy = (s_maxl <= (uint32_t)kWarpSortMax && s_sq <= (uint32_t)kWarpSortMean * m) ? 1u : 2u;
+  if (tid == 0 && (s_maxl > (uint32_t)kMaxGroup || s_sq > (uint32_t)kMeanGroupMax * m)) heavy = 1;
 
   FS_LPH(1);  // 1: scan
   // ---- counting scatter of the composites (order inside a group is fixed below)
@@ -1487,18 +1427,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
 
   FS_LPH(3);  // 3: ranks
   uint16_t* pfinal = fin;
-  const bool in_place = heavy == 1;  // the groups are sorted where they lie: position j holds slot j
-  if (in_place) {
-    for (uint32_t g = warp; g < ngroups; g += kLocalWarps) {
-      const uint32_t gs = g ? cnt16[g - 1] : 0u, L = (uint32_t)cnt16[g] - gs;
-      if (L <= 1) continue;
-      if (kWarpSortMax >= 32 && L <= 32) warp_sort_group<1>(ck, gs, L);
-      else if (kWarpSortMax >= 64 && L <= 64) warp_sort_group<2>(ck, gs, L);
-      else if (kWarpSortMax >= 128 && L <= 128) warp_sort_group<4>(ck, gs, L);
-      else if (kWarpSortMax >= 256) warp_sort_group<8>(ck, gs, L);
-    }
-    __syncthreads();
-  } else if (heavy) {
+  if (heavy) {
     // ---- slow path: stable LSD over the varying 8-bit digits of the R bits
     uint16_t* pa = perm;
     uint16_t* pb = reinterpret_cast<uint16_t*>(smem_raw + Lay::perm_b);
@@ -1522,8 +1451,8 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
     const uint64_t varying = or_all ^ and_all;
     const uint32_t chunk = ((m + kLocalWarps - 1) / kLocalWarps + 31) & ~31u;
     const uint32_t c0 = min(warp * chunk, m), c1 = min(c0 + chunk, m);
-    for (int sh = 0; sh < R; sh += kRadixBits) {
-      if (((varying >> sh) & 0xFFu) == 0) continue;  // uniform digit: the pass is the identity
+    // One stable pass pa -> pb by the digit (ck[p] >> shift) & dmask (dmask <= 255).
+    auto lsd_pass = [&](int shift, uint32_t dmask) {
       for (int i = tid; i < kLocalWarps * kRadix; i += kLocalThreads) wh16[i] = 0;
       __syncthreads();
       uint16_t* whw = wh16 + warp * kRadix;
@@ -1531,7 +1460,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
       for (uint32_t j0 = c0; j0 < c1; j0 += 32) {
         const uint32_t j = j0 + lane;
         const bool valid = j < c1;
-        const uint32_t dg = valid ? (uint32_t)(ck[pa[j]] >> (kIdxBits + sh)) & 0xFFu : 0u;
+        const uint32_t dg = valid ? (uint32_t)(ck[pa[j]] >> shift) & dmask : 0u;
         const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
         if (valid && lane == 31 - __clz(peers)) whw[dg] = (uint16_t)(whw[dg] + __popc(peers));
         __syncwarp();
@@ -1562,7 +1491,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
         const uint32_t j = j0 + lane;
         const bool valid = j < c1;
         const uint16_t p = valid ? pa[j] : (uint16_t)0;
-        const uint32_t dg = valid ? (uint32_t)(ck[p] >> (kIdxBits + sh)) & 0xFFu : 0u;
+        const uint32_t dg = valid ? (uint32_t)(ck[p] >> shift) & dmask : 0u;
         const uint32_t peers = match_digit8(dg, __ballot_sync(kFull, valid));
         const uint32_t leader = 31 - __clz(peers);
         uint32_t old = 0;
@@ -1578,8 +1507,121 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
       uint16_t* t = pa;
       pa = pb;
       pb = t;
+    };
+    bool done = false;
+#ifndef FS_GROUP_FIRST
+#define FS_GROUP_FIRST 1
+#endif
+    if (FS_GROUP_FIRST && ngroups > 1) {
+      // Group digit first: two stable passes by the counting digit put every group
+      // in arrival order, so a group whose keys are all equal (repeated keys) is
+      // already sorted; a group of a few values (<= kGroupValuesMax) is ordered by
+      // one stable compaction sweep per value; more values send the bin to the
+      // full LSD over the varying digits.
+      const int gb = cb < 8 ? cb : 8;
+      lsd_pass(cshift, (1u << gb) - 1u);
+      if (cb > 8) lsd_pass(cshift + 8, (1u << (cb - 8)) - 1u);
+#if FS_GROUP_FIRST == 2  // timing experiment only: assume every group holds one value
+      pfinal = pa;
+      done = true;
+      if (false)
+#endif
+      {
+      if (tid == 0) s_fallback = 0;
+      __syncthreads();
+      // Group boundaries (the counters under perm_b are gone): a group starts where
+      // the digit changes along pa.  A warp handles the groups that start in its
+      // chunk [c0, c1), scanning past c1 for the end of its last one.
+      auto gof = [&](uint32_t q) -> uint32_t { return (uint32_t)(ck[pa[q]] >> cshift) & (ngroups - 1u); };
+      auto handle = [&](uint32_t gs, uint32_t ge) {  // warp-wide
+        uint64_t mn = ~0ull, mx = 0;
+        for (uint32_t q = gs + lane; q < ge; q += 32) {
+          const uint64_t kp = ck[pa[q]] >> kIdxBits;
+          mn = kp < mn ? kp : mn;
+          mx = kp > mx ? kp : mx;
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+          const uint64_t a = __shfl_xor_sync(kFull, mn, d), b = __shfl_xor_sync(kFull, mx, d);
+          mn = a < mn ? a : mn;
+          mx = b > mx ? b : mx;
+        }
+        if (mn == mx) {  // one value: arrival order is the order
+          for (uint32_t q = gs + lane; q < ge; q += 32) pb[q] = pa[q];
+          return;
+        }
+        // a few values: one stable compaction sweep per value, smallest first
+        // (the group is in arrival order); more than kGroupValuesMax values: the
+        // bin takes the full LSD
+        uint64_t cur = mn;
+        uint32_t base = gs;
+        for (int it = 0;; ++it) {
+          if (it == kGroupValuesMax) {
+            if (lane == 0) s_fallback = 1;
+            return;
+          }
+          uint64_t nxt = ~0ull;
+          for (uint32_t q0 = gs; q0 < ge; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const uint64_t kp = q < ge ? ck[pa[q]] >> kIdxBits : ~0ull;
+            const bool eq = q < ge && kp == cur;
+            const uint32_t bal = __ballot_sync(kFull, eq);
+            if (eq) pb[base + __popc(bal & lanemask_lt())] = pa[q];
+            base += __popc(bal);
+            nxt = (kp > cur && kp < nxt) ? kp : nxt;
+          }
+#pragma unroll
+          for (int d = 16; d >= 1; d >>= 1) {
+            const uint64_t a = __shfl_xor_sync(kFull, nxt, d);
+            nxt = a < nxt ? a : nxt;
+          }
+          if (nxt == ~0ull) return;
+          cur = nxt;
+        }
+      };
+      if (c0 < c1) {
+        constexpr uint32_t kNone = 0xFFFFFFFFu;
+        uint32_t open = kNone;                               // start of the group being scanned
+        uint32_t gprev = c0 > 0 ? gof(c0 - 1) : kNone;       // digit just before this block
+        bool stop = false;
+        for (uint32_t q0 = c0; q0 <= m && !stop; q0 += 32) {
+          const uint32_t q = q0 + lane;
+          const uint32_t gq = q < m ? gof(q) : 0xFFFFFFFEu;  // position m closes the last group
+          uint32_t gl = __shfl_up_sync(kFull, gq, 1);
+          if (lane == 0) gl = gprev;
+          uint32_t starts = __ballot_sync(kFull, q <= m && gq != gl);
+          gprev = __shfl_sync(kFull, gq, 31);
+          while (starts) {
+            const uint32_t t = q0 + (uint32_t)(__ffs(starts) - 1);
+            starts &= starts - 1;
+            if (open != kNone) handle(open, t);
+            open = kNone;
+            if (t < c1 && t < m) {
+              open = t;
+            } else {
+              stop = true;
+              break;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (!s_fallback) {
+        pfinal = pb;
+        done = true;
+      } else {  // back to arrival order for the full LSD
+        for (uint32_t j = tid; j < m; j += kLocalThreads) pa[ck[j] & ((1u << kIdxBits) - 1)] = (uint16_t)j;
+        __syncthreads();
+      }
+      }
     }
-    pfinal = pa;
+    if (!done) {
+      for (int sh = 0; sh < R; sh += kRadixBits) {
+        if (((varying >> sh) & 0xFFu) == 0) continue;  // uniform digit: the pass is the identity
+        lsd_pass(kIdxBits + sh, 0xFFu);
+      }
+      pfinal = pa;
+    }
   }
 
   FS_LPH(4);  // 4: slow path (heavy bins only)
@@ -1588,7 +1630,7 @@ __device__ __forceinline__ void sort_bin(const K* kin, const uint32_t* vin, K* k
   {
 #pragma unroll 4
     for (uint32_t j = tid; j < m; j += kLocalThreads) {
-      const uint64_t c = ck[in_place ? j : pfinal[j]];
+      const uint64_t c = ck[pfinal[j]];
       kout[b0 + j] = top + (K)(c >> kIdxBits);
       pfinal[j] = (uint16_t)(c & ((1u << kIdxBits) - 1));
     }

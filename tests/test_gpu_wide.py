@@ -179,6 +179,28 @@ def test_msd_pairs_repeated_keys(cuda, copies):
     np.testing.assert_array_equal(to_host(vo), ev)
 
 
+@pytest.mark.parametrize("low_values", [1, 3, 16, 17, 0])
+def test_msd_pairs_slow_path_groups(cuda, low_values):
+    """~8,192-key bins whose keys share the counting digit (the 12 bits below the
+    16-bit bin) and differ only in the low 36 bits: every bin is one group, so it
+    takes the slow path; it sorts by the counting digit first, then finishes a
+    group of <= 16 distinct keys by stable value sweeps (1, 3, 16 values) or
+    falls back to the full LSD (17 values; 0 = all-random low bits)."""
+    n = 1 << 21
+    tops = datagen.gen_u64(256, seed=31) & np.uint64(0xFFFFFFF000000000)
+    top = tops[datagen.gen_u64(n, seed=32) % np.uint64(256)]
+    rnd = datagen.gen_u64(n, seed=33) & np.uint64((1 << 36) - 1)
+    if low_values:
+        vals = datagen.gen_u64(low_values, seed=34) & np.uint64((1 << 36) - 1)
+        rnd = vals[datagen.gen_u64(n, seed=35) % np.uint64(low_values)]
+    k = top | rnd
+    v = datagen.iota_u32(n)
+    ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda))
+    ek, ev = oracle.sort_pairs_u64_u32(k, v)
+    np.testing.assert_array_equal(to_host(ko), ek)
+    np.testing.assert_array_equal(to_host(vo), ev)
+
+
 def _check_pairs(cuda, k, key_bits=64):
     v = datagen.iota_u32(len(k))
     ko, vo = fs.sort_pairs(to_dev(k, cuda), to_dev(v, cuda), key_bits=key_bits)
