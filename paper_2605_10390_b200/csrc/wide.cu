@@ -1232,12 +1232,16 @@ static_assert(LocalSmemLayout::total <= 113 * 1024, "two CTAs per SM");
 // key - top.  Keys become composites c = (key - top) << 14 | i
 // (i = arrival index inside the bin), all distinct, so ordering composites is
 // the stable order.
-//  fast path: counting sort by the top `cb` of the R bits (cb = ceil(log2 m),
-//    <= 12; groups of ~1-2 keys) with shared atomics, then every key's final
-//    position = group start + #composites of its group below its own (groups
-//    <= 32 keys), written straight to the output;
-//  slow path (a group > 32 keys: low-entropy bins): stable LSD over the varying
-//    8-bit digits of the R bits on the permutation (warp multisplit ranks).
+//  counting sort by the top `cb` of the R bits (cb = ceil(log2 m), <= 12;
+//    groups of ~1-2 keys for distinct keys) with shared atomics; then, chosen
+//    per bin from the group sizes (kMaxGroup, kMeanGroupMax):
+//  fast path: every key's final position = group start + #composites of its
+//    group below its own;
+//  slow path (large groups: repeated keys, low-entropy bins): stable passes by
+//    the counting digit on a permutation (warp multisplit ranks), after which a
+//    group of one value is final and a group of <= kGroupValuesMax values is
+//    finished by value sweeps; otherwise a stable LSD over the varying 8-bit
+//    digits of the R bits.
 // Output: kout[b0 + j] = top + (c_j >> 14), vout[b0 + j] = vin[b0 + i_j]; kin == kout
 // (in place) is allowed: every key is in registers before the first store.
 template <typename K, bool kHasValues, class Cfg = BigCfg>
