@@ -1,7 +1,9 @@
 """Time fs_sort_pairs_u64_u32 on skewed 64-bit key distributions (oversize 16-bit
-bins: the MSD recursion) for each library in scripts/microbench/variants/*.so
-(or the in-tree library), checking the result's order and that it is a
-permutation of the input pairs.  n = argv[1] (default 2^28)."""
+bins: the MSD recursion; repeated keys: the per-bin sort's slow path) for each
+library in scripts/microbench/variants/*.so (or the in-tree library), checking
+the result's order, that it is a permutation of the input pairs and stability.
+n = argv[1] (default 2^28); argv[2] = comma-separated kinds: uniform, hot16x25,
+hot1x50, clustered, lt2^B (keys < 2^B), dupM (each key ~M times, M a power of 2)."""
 import ctypes, glob, os, statistics, sys
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
