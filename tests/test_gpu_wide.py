@@ -159,17 +159,18 @@ def test_msd_pairs_heavy_bins(cuda, distinct_low):
     np.testing.assert_array_equal(to_host(vo), ev)
 
 
+@pytest.mark.parametrize("bins", [256, 1500])
 @pytest.mark.parametrize("copies", [2, 8, 16, 32, 64, 200])
-def test_msd_pairs_repeated_keys(cuda, copies):
+def test_msd_pairs_repeated_keys(cuda, copies, bins):
     """Every key repeated ~`copies` times inside ~8,192-key 16-bit bins (256 bins
-    used, so k_local_sort sorts them): the per-bin group-size test sends a bin to
-    the rank loop (groups <= kMaxGroup, key-weighted mean <= kMeanGroupMax) or to
-    the slow path; with values = arrival indices, either must give the oracle's
-    stable order."""
+    used: k_local_sort) or ~1,400-key bins (1,500 used: k_local_mid): the per-bin
+    group-size test sends a bin to the rank loop (groups <= kMaxGroup,
+    key-weighted mean <= kMeanGroupMax) or to the slow path; with values =
+    arrival indices, either must give the oracle's stable order."""
     n = 1 << 21
-    tops = datagen.gen_u64(256, seed=21) & np.uint64(0xFFFF000000000000)
+    tops = datagen.gen_u64(bins, seed=21) & np.uint64(0xFFFF000000000000)
     distinct = n // copies
-    base = tops[datagen.gen_u64(distinct, seed=22) % np.uint64(256)] | \
+    base = tops[datagen.gen_u64(distinct, seed=22) % np.uint64(bins)] | \
         (datagen.gen_u64(distinct, seed=23) & np.uint64((1 << 48) - 1))
     k = base[datagen.gen_u64(n, seed=24) % np.uint64(distinct)]
     v = datagen.iota_u32(n)
