@@ -180,6 +180,30 @@ def test_msd_pairs_repeated_keys(cuda, copies, bins):
     np.testing.assert_array_equal(to_host(vo), ev)
 
 
+@pytest.mark.parametrize("width", [32, 64])
+@pytest.mark.parametrize("copies", [8, 64, 200])
+def test_msd_keys_repeated(cuda, copies, width):
+    """Keys-only sorts (fs_sort_keys_u32 / u64: the per-bin sort without values)
+    of keys repeated ~`copies` times in ~8,192-key bins: rank loop, digit-first
+    slow path with value sweeps, against the oracle."""
+    n = 1 << 21
+    if width == 64:
+        tops = datagen.gen_u64(256, seed=41) & np.uint64(0xFFFF000000000000)
+        distinct = n // copies
+        base = tops[datagen.gen_u64(distinct, seed=42) % np.uint64(256)] | \
+            (datagen.gen_u64(distinct, seed=43) & np.uint64((1 << 48) - 1))
+        k = base[datagen.gen_u64(n, seed=44) % np.uint64(distinct)]
+        want = oracle.sort_keys_u64(k)
+    else:
+        tops = datagen.gen_u32(256, seed=41) & np.uint32(0xFFFF0000)
+        distinct = n // copies
+        base = tops[datagen.gen_u32(distinct, seed=42) % np.uint32(256)] | \
+            (datagen.gen_u32(distinct, seed=43) & np.uint32(0xFFFF))
+        k = base[datagen.gen_u32(n, seed=44) % np.uint32(distinct)]
+        want = oracle.sort_keys_u32(k)
+    np.testing.assert_array_equal(to_host(fs.sort_keys(to_dev(k, cuda))), want)
+
+
 @pytest.mark.parametrize("low_values", [1, 3, 16, 17, 0])
 def test_msd_pairs_slow_path_groups(cuda, low_values):
     """~8,192-key bins whose keys share the counting digit (the 12 bits below the
