@@ -203,7 +203,7 @@ def worker(rank, world, port, outdir, peer_bufs):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_distributed_sort_matches_oracle(tmp_path, world):
     """Modes A, B and P (expand-to-peer), four distributions (uneven and empty shards included)."""
     import datagen
@@ -273,7 +273,7 @@ def pair_worker(rank, world, port, outdir, peer_bufs):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_distributed_pairs_match_oracle(tmp_path, world):
     """Pairs, modes A (local sort, all_to_all, local sort) and P (classes, stores into
     the owners' buffers, one sort): exact splitters from one all-reduced 16-bit
