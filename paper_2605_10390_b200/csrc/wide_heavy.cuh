@@ -40,6 +40,11 @@
 // the copy pieces.
 #pragma once
 
+#ifndef FS_HEAVY_C_UNROLL  // phase C: chunk-count loads in flight per thread (one CTA walks a segment's chunks)
+#define FS_HEAVY_C_UNROLL 32
+#endif
+constexpr int kHeavyCUnroll = FS_HEAVY_C_UNROLL;
+
 // (The records HeavySeg / HeavyItem / HeavyCtl and the capacities are defined in
 // wide.cu next to MsdPlan: k_msd_plan seeds the first level.)
 
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
     for (uint32_t s = blockIdx.x; s < S; s += gridDim.x) {
       const HeavySeg sg = load_seg(segs + s);
       uint64_t T = 0;
-#pragma unroll 8
+#pragma unroll kHeavyCUnroll
       for (uint32_t i = 0; i < sg.nc; ++i) T += __ldcg(&a.chist[(uint64_t)(sg.c0 + i) * kRadix + d]);
       const int single = l2 ? 0 : __syncthreads_or(T == sg.count);
       if (single) {  // one digit: nothing moves at this level
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 2) k_heavy(HeavyArgs<K> a) {
       }
       const uint64_t excl = block_excl_scan256(T, wsum64);
       uint64_t run = sg.begin + excl;
-#pragma unroll 8
+#pragma unroll kHeavyCUnroll
       for (uint32_t i = 0; i < sg.nc; ++i) {
         const uint64_t ci = (uint64_t)(sg.c0 + i) * kRadix + d;
         a.cbase[ci] = run;
