@@ -130,6 +130,12 @@ constexpr int kMaxPasses = 8;
 #ifndef FS_L1_HALVES
 #define FS_L1_HALVES 1
 #endif
+// k_scatter reads its predecessor's status word early (1: when it publishes its
+// own counts; 2: at tile start) and uses it at the lookback if it already held
+// the inclusive prefix, saving the lookback's L2 round trip (0: off).
+#ifndef FS_SCATTER_EARLY_LOOK
+#define FS_SCATTER_EARLY_LOOK 1
+#endif
 #ifndef FS_SCATTER_STORE_UNROLL
 #define FS_SCATTER_STORE_UNROLL 1
 #endif
@@ -1028,6 +1034,11 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     // Digit threads fetch their global digit base now; it is needed only after the lookback.
     const uint32_t d = tid;
     const uint64_t dbase = d < kRadix ? __ldg(base_tab + (uint64_t)ti.seg * base_ss + (uint64_t)d * base_ds) : 0ull;
+    unsigned long long pre = 0;  // the predecessor's status word, read early (FS_SCATTER_EARLY_LOOK)
+#if FS_SCATTER_EARLY_LOOK == 2
+    if (d < kRadix && !ti.first)
+      pre = ld_relaxed_u64(a.status + (uint64_t)((int64_t)ti.tile - (int64_t)ti.stride) * kRadix + d);
+#endif
 
     FS_PH(0);  // 0: fetch + wait for the tile's bytes
     // ---- items: warp w holds tile elements [256 w, 256 w + 256), item i of lane l = 256 w + 32 i + l
@@ -1066,6 +1077,10 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     // ---- tile digit counts (thread = digit); publish; per-warp offsets
     uint32_t cnt = 0;
     unsigned long long* st = a.status + (uint64_t)ti.tile * kRadix + d;
+#if FS_SCATTER_EARLY_LOOK == 1
+    if (d < kRadix && !ti.first)
+      pre = ld_relaxed_u64(a.status + (uint64_t)((int64_t)ti.tile - (int64_t)ti.stride) * kRadix + d);
+#endif
     if (d < kRadix) {
 #pragma unroll
       for (int w = 0; w < kSWarps; ++w) {
@@ -1127,7 +1142,11 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
         // the older rows have left L2.)
         bool done = false;
         {
-          unsigned long long s = ld_relaxed_u64(a.status + (uint64_t)t * kRadix + d);
+          // the word read at publish time (one L2 round trip earlier) if it already
+          // held the inclusive prefix, else a fresh read
+          unsigned long long s = pre;
+          if (!FS_SCATTER_EARLY_LOOK || (s & (0x3Full << kTagShift)) != a.tag || (s >> 62) != 2)
+            s = ld_relaxed_u64(a.status + (uint64_t)t * kRadix + d);
           while ((s & (0x3Full << kTagShift)) != a.tag || (s >> 62) == 0)  // not yet published
             s = ld_relaxed_u64(a.status + (uint64_t)t * kRadix + d);
           excl += s & kStValue;
