@@ -136,6 +136,9 @@ constexpr int kMaxPasses = 8;
 #ifndef FS_SCATTER_EARLY_LOOK
 #define FS_SCATTER_EARLY_LOOK 1
 #endif
+#ifndef FS_SCATTER_L2PF  // k_scatter: bulk-prefetch the tile after next into L2 in these modes (bit mask)
+#define FS_SCATTER_L2PF 4   // mode 2 (MSD level 2) only
+#endif
 #ifndef FS_SCATTER_STORE_UNROLL
 #define FS_SCATTER_STORE_UNROLL 1
 #endif
@@ -1072,7 +1075,12 @@ __global__ void __launch_bounds__(kSThreads, FS_SCATTER_MINB) k_scatter(ScatterA
     }
     __syncthreads();
 
-    if (tid == 0) prefetch_spare();
+    // L2 bulk prefetch of the tile after next, level 2 only (FS_SCATTER_L2PF: bit m
+    // = pass mode m).  Round 1 measured it neutral everywhere; with the round-2
+    // loop it costs level 1 ~0.09 ms per c5 sort (3.54 vs 3.45 ms without) but
+    // helps level 2 on uneven buckets (16 hot bins: 2.70 vs 2.97 ms);
+    // profiles/r02f/wide_variants_l2pf.txt.
+    if (((FS_SCATTER_L2PF >> a.mode) & 1) && tid == 0) prefetch_spare();
     FS_PH(1);  // 1: load items + rank + barrier
     // ---- tile digit counts (thread = digit); publish; per-warp offsets
     uint32_t cnt = 0;
