@@ -331,14 +331,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_hist16(HistArgs a) {
   const uint4* __restrict__ vec = reinterpret_cast<const uint4*>(a.keys + a.head);
   const uint64_t nvec = a.nvec;
   // Work is split into groups of kUnroll x 1024 vectors (16,384 keys).  Most
-  // groups are assigned statically (grid-strided); the last 1/8 are handed out
+  // groups are assigned statically (grid-strided); the last 1/16 are handed out
   // dynamically in warp-sized chunks (2,048 keys) from a global counter,
   // because SMs run the atomic-bound loop at rates ~8% apart (hist_trace:
   // per-CTA loop 115-125 us on 2^28 keys).  Per-warp tickets need no CTA
   // barrier, so no warp waits on another's loads.
   constexpr uint64_t kGroupVec = (uint64_t)kUnroll * kThreads;
 #ifndef FS_HIST_CHUNK_ITERS  // scripts/microbench sweeps
-#define FS_HIST_CHUNK_ITERS 8
+#define FS_HIST_CHUNK_ITERS 4
 #endif
 #ifndef FS_HIST_DYN_DIV
 #define FS_HIST_DYN_DIV 16
