@@ -12,7 +12,7 @@ PKG       := paper_2605_10390_b200
 CSRC      := $(PKG)/csrc
 KERNEL_SRCS := $(CSRC)/abi.cu $(CSRC)/hist16.cu $(CSRC)/scan.cu $(CSRC)/expand16.cu \
                $(CSRC)/wide.cu $(CSRC)/partition.cu $(CSRC)/host_stream.cu $(CSRC)/trie.cu $(CSRC)/peer.cu \
-               $(CSRC)/small16.cu $(CSRC)/exchange.cu
+               $(CSRC)/small16.cu $(CSRC)/exchange.cu $(CSRC)/nvls.cu
 KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) include/fractalsort.h
 KERNEL_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(KERNEL_SRCS))
 

@@ -643,6 +643,8 @@ def run_fs(args, rank, world, local_rank):
         line["c4_strong"] = c4_strong_block(args, L, _lib, rank, world, dev, dist, peak)
         line["mode_A"] = exchange_block("A", keys, rank, world, dev, dist, args)
         line["mode_P"] = exchange_block("P", keys, rank, world, dev, dist, args)
+        if os.environ.get("FS_BENCH_SHARE_GPU") != "1":  # its in-kernel barrier needs one GPU per rank
+            line["mode_N"] = exchange_block("N", keys, rank, world, dev, dist, args)
         del keys
         torch.cuda.empty_cache()
         line["pairs_P"] = pairs_block("P", rank, world, dev, dist, args)
@@ -689,12 +691,13 @@ def c4_strong_block(args, L, _lib, rank, world, dev, dist, peak):
 def exchange_block(mode, keys, rank, world, dev, dist, args):
     """Payload exchange of the c2 shards: mode A (NCCL all-to-all of the key bytes
     after a local sort, then a local sort) or mode P (every rank's keys stored
-    straight to their final positions in the owners' buffers over NVLink)."""
+    straight to their final positions in the owners' buffers over NVLink); mode N
+    is mode B with the prefix all-reduce done by the NVSwitch (multicast)."""
     import torch
 
     from paper_2605_10390_b200 import dist as fsd
     try:
-        peers = fsd.PeerBuffers(dev) if mode == "P" else None
+        peers = fsd.PeerBuffers(dev) if mode == "P" else (fsd.MulticastBuffer(65536 + 128, dev) if mode == "N" else None)
         ev = {"x0": torch.cuda.Event(enable_timing=True), "x1": torch.cuda.Event(enable_timing=True)}
         stats = {}
         steps = max(2, min(args.steps, 5))
@@ -712,6 +715,8 @@ def exchange_block(mode, keys, rank, world, dev, dist, args):
                 totals.append(a.elapsed_time(b))
         x_ms = max_over_ranks(statistics.median(xs), dev, dist)
         t_ms = max_over_ranks(statistics.median(totals), dev, dist)
+        if mode == "N":  # the reduced two-level prefix each rank reads through the switch
+            stats["sent_bytes"] = (65536 + 128) * 8
         sent = max_over_ranks(float(stats.get("sent_bytes", 0)), dev, dist)
         n_total = keys.numel() * world
         blk = {"mode": mode, "keys_total": n_total, "ms_per_sort": round(t_ms, 4),
@@ -719,8 +724,11 @@ def exchange_block(mode, keys, rank, world, dev, dist, args):
                "exchange_ms": round(x_ms, 4), "sent_bytes_per_rank": int(sent),
                "nvlink_GBps_per_rank": round(sent / (x_ms * 1e-3) / 1e9, 1),
                "frac_of_900GBps": round(sent / (x_ms * 1e-3) / 1e9 / NVLINK_GBPS, 4),
-               "exchange": ("NCCL all_to_all_single of the key bytes" if mode == "A" else
-                            "fs_expand_to_peers_u16: stores into the owners' CUDA-IPC-mapped buffers"),
+               "exchange": {"A": "NCCL all_to_all_single of the key bytes",
+                            "P": "fs_expand_to_peers_u16: stores into the owners' CUDA-IPC-mapped buffers",
+                            "N": "fs_allreduce_multicast_u64: the two-level prefix summed by the NVSwitch "
+                                 "(multimem.ld_reduce) with the kernel's own barrier; no payload exchange "
+                                 "(mode B with NVLS instead of NCCL)"}[mode],
                "timing": f"median of {steps} sorts, max over ranks; exchange = CUDA events around it"}
         if not args.no_verify:
             blk["verified"] = all_ok(verify_range(res, begin, global_hist(keys, dev, dist)), dev, dist)
@@ -768,6 +776,8 @@ def pairs_block(mode, rank, world, dev, dist, args):
                 totals.append(a.elapsed_time(b))
         x_ms = max_over_ranks(statistics.median(xs), dev, dist)
         t_ms = max_over_ranks(statistics.median(totals), dev, dist)
+        if mode == "N":  # the reduced two-level prefix each rank reads through the switch
+            stats["sent_bytes"] = (65536 + 128) * 8
         sent = max_over_ranks(float(stats.get("sent_bytes", 0)), dev, dist)
         blk = {"mode": mode, "pairs_total": N, "ms_per_sort": round(t_ms, 4),
                "value": round(N / (t_ms * 1e-3) / 1e9, 3), "unit": "Gpairs/s", "scaling": "strong",

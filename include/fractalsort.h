@@ -276,6 +276,30 @@ size_t fs_expand_to_peers_u16_temp_bytes(uint64_t nbins, int G);
 fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_t nbins, uint16_t* const* dest,
                                  void* temp, size_t temp_bytes, fs_stream_t stream);
 
+/* fs_allreduce_multicast_u64: the cross-GPU histogram merge through NVSwitch
+ * multicast (NVLS; SURVEY.md §8(f) NEXT-2, row a3 across GPUs): the Global
+ * Histogram Update of PAPER.md:91-92 (§III.B) over G ranks.
+ * dst[i] = sum over ranks r of src_r[i] for i < count, where src_mc is the
+ * MULTICAST address (cuMulticastCreate + cuMulticastBindMem, every rank's own
+ * physical memory bound at the same offset) of the ranks' u64 arrays: each
+ * element is one multimem.ld_reduce.add, summed by the switch.  dst: count u64
+ * of ordinary device memory of the calling rank.  The call contains the
+ * barrier the reduction needs: it adds 1 to the u32 flag in every rank's copy
+ * (flag_mc: its multicast address, multimem.red.release) and waits until this
+ * rank's copy (flag_local: the same word through the rank's unicast mapping)
+ * reaches `target` (wrap-safe compare; callers pass G x the number of calls made
+ * so far on this flag, this one included), so no rank reads before every rank's
+ * src_r is complete.  A caller that rewrites src before every rank has read it
+ * must alternate two src regions by call parity.  All pointers device, 8-byte
+ * (flags 4-byte) aligned; src_mc and dst must not overlap.  Every rank of the
+ * multicast group must make the matching call, or the others wait forever (as
+ * with any collective).  count = 0 still arrives and waits (a pure barrier).
+ * Errors: FS_ERR_INVALID_ARGUMENT for NULL / misaligned / overlapping
+ * arguments; FS_ERR_CUDA if the launch fails (e.g. src_mc not a multicast
+ * mapping surfaces as an asynchronous fault at the caller's next sync). */
+fs_status fs_allreduce_multicast_u64(const uint64_t* src_mc, uint64_t* dst, uint64_t count, uint32_t* flag_mc,
+                                     const uint32_t* flag_local, uint32_t target, fs_stream_t stream);
+
 /* ----------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use, and the out-of-core path of Batch
  * Size Selection / Batch Counter Update): sorts n u16 keys

@@ -23,7 +23,7 @@ __all__ = [
     "sort_keys_u16_host", "sort_keys_u16_host_work_bytes", "FractalSortError", "lib",
     "histogram_prefix_u16", "expand_prefix_u16", "expand_to_peers_u16", "bound_u64", "trie_levels", "PackedTrie",
     "trie_pack", "get_item", "get_index", "hist_merge", "histogram16_u64", "select_bins_u64",
-    "digit_counts_sorted_u64", "PairExchange",
+    "digit_counts_sorted_u64", "PairExchange", "allreduce_multicast_u64",
 ]
 
 _TEMP_ALIGN = 256
@@ -127,21 +127,36 @@ def histogram_u16(keys: torch.Tensor, key_bits: int = 16, hist: torch.Tensor | N
     return hist
 
 
-def histogram_prefix_u16(keys: torch.Tensor, prefix2: torch.Tensor | None = None) -> torch.Tensor:
+def histogram_prefix_u16(keys: torch.Tensor, prefix2: torch.Tensor | None = None, out_ptr: int | None = None):
     """The sort's two-level prefix of keys: 65,536 slice-local prefixes + 128 slice totals, int64
-    (fs_histogram_prefix_u16); sums over ranks stay in the same form."""
+    (fs_histogram_prefix_u16); sums over ranks stay in the same form.  ``out_ptr``: write them
+    to this raw device address instead (e.g. a multicast-bound buffer, dist.MulticastBuffer)
+    and return None."""
     dev = _require_cuda(keys)
     if keys.dtype != torch.uint16:
         raise TypeError("histogram_prefix_u16 expects uint16 keys")
-    if prefix2 is None:
+    if out_ptr is None and prefix2 is None:
         prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
     n = keys.numel()
     L = lib()
     with torch.cuda.device(dev):
         temp = _temp(L.fs_histogram_u16_temp_bytes(n), dev)
-        check(L.fs_histogram_prefix_u16(keys.data_ptr(), n, prefix2.data_ptr(), temp.data_ptr(), temp.numel(),
-                                        _stream(dev)), "fs_histogram_prefix_u16")
-    return prefix2
+        check(L.fs_histogram_prefix_u16(keys.data_ptr(), n, out_ptr if out_ptr is not None else prefix2.data_ptr(),
+                                        temp.data_ptr(), temp.numel(), _stream(dev)), "fs_histogram_prefix_u16")
+    return None if out_ptr is not None else prefix2
+
+
+def allreduce_multicast_u64(src_mc: int, dst: torch.Tensor, flag_mc: int, flag_local: int, target: int):
+    """dst[i] = sum over ranks of their src[i] (int64/uint64 dst, i < dst.numel()), read through the
+    multicast address src_mc by multimem.ld_reduce, with the call's cross-GPU barrier on the
+    flag word (fs_allreduce_multicast_u64; addresses from dist.MulticastBuffer)."""
+    dev = _require_cuda(dst)
+    if dst.dtype not in (torch.int64, torch.uint64) or not dst.is_contiguous():
+        raise TypeError("dst must be a contiguous 64-bit integer tensor")
+    with torch.cuda.device(dev):
+        check(lib().fs_allreduce_multicast_u64(src_mc, dst.data_ptr(), dst.numel(), flag_mc, flag_local,
+                                               target & 0xFFFFFFFF, _stream(dev)), "fs_allreduce_multicast_u64")
+    return dst
 
 
 def expand_prefix_u16(prefix2: torch.Tensor, out_begin: int, out_end: int, out: torch.Tensor | None = None):

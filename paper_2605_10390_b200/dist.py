@@ -24,11 +24,21 @@ mode "P" (fused expand-to-peer): all_gather of the
     fs_expand_to_peers_u16); a barrier ends the exchange.  The payload crosses
     NVLink once and no rank sorts anything.
 
+mode "N" (NVLS): mode B with the all_reduce done by the
+    NVSwitch.  Each rank's histogram kernel writes its two-level prefix straight
+    into its own GPU memory bound into one multicast object (MulticastBuffer);
+    fs_allreduce_multicast_u64 then reads the sum over ranks through the
+    multicast address (multimem.ld_reduce: the switch adds the G copies) after a
+    barrier carried by the same kernel (multimem.red on a flag word).  No NCCL
+    kernel, no staging copy; 513 KiB per rank read through the switch.
+
 ``ops`` supplies the local steps.  The default, CudaOps, calls the library's
 kernels through the binding; the gloo tests on CPU inject their own stand-ins
 (from tests/), which exercises exactly this module's orchestration.
 """
 from __future__ import annotations
+
+import os
 
 import torch
 import torch.distributed as dist
@@ -97,6 +107,14 @@ class CudaOps:
         from . import PairExchange
         return PairExchange(keys, vals, splitters, G)
 
+    def histogram_prefix_u16_to(self, keys, out_ptr):
+        from . import histogram_prefix_u16
+        histogram_prefix_u16(keys, out_ptr=out_ptr)
+
+    def allreduce_multicast(self, src_mc, dst, flag_mc, flag_local, target):
+        from . import allreduce_multicast_u64
+        return allreduce_multicast_u64(src_mc, dst, flag_mc, flag_local, target)
+
     def synchronize(self, device):
         torch.cuda.synchronize(device)
 
@@ -124,6 +142,144 @@ class PeerBuffers:
             self.views = [v.view(self.dtype) for v in views]
             self.capacity = per_rank
         return self.views
+
+
+def share_fd(fd, group=None):
+    """Rank 0's file descriptor ``fd``, duplicated into every rank of ``group``
+    (SCM_RIGHTS over an abstract Unix socket; the socket name travels through
+    the process group).  Returns the local descriptor (rank 0: ``fd`` itself).
+    Used for the multicast object's POSIX handle (MulticastBuffer)."""
+    import socket
+    import uuid
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return fd
+    name = [None]
+    srv = None
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        addr = "\0fractalsort-fd-" + uuid.uuid4().hex
+        srv.bind(addr)
+        srv.listen(world)
+        name = [addr]
+    dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    if rank == 0:
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"f"], [fd])
+                    conn.recv(1)                                   # the peer holds its copy
+        finally:
+            srv.close()
+        return fd
+    with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.connect(name[0])
+        _, fds, _, _ = socket.recv_fds(c, 1, 1)
+        c.sendall(b"k")
+    if len(fds) != 1:
+        raise RuntimeError(f"share_fd: rank {rank} received {len(fds)} descriptors")
+    return fds[0]
+
+
+class MulticastBuffer:
+    """``count`` u64 per half, two halves (alternated by call parity), and a u32
+    flag, in every rank's GPU memory, all bound at the same offsets into ONE
+    NVSwitch multicast object (driver API through cuda-python: cuMulticastCreate
+    on rank 0, POSIX-fd export shared with share_fd, cuMulticastAddDevice on
+    every rank, a barrier, cuMemCreate + cuMulticastBindMem, then unicast and
+    multicast virtual mappings).  ``step()`` returns the addresses of the next
+    call of fs_allreduce_multicast_u64: (local half pointer, multicast half
+    pointer, flag multicast pointer, flag local pointer, target)."""
+
+    def __init__(self, count: int, device, group=None):
+        from cuda.bindings import driver as cu
+        self._cu, self.count, self.group = cu, int(count), group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.device = torch.device(device)
+        torch.cuda.set_device(self.device)
+        torch.cuda.synchronize(self.device)            # the primary context is current on this thread
+
+        def ok(res, what):
+            err = res[0] if isinstance(res, tuple) else res
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(f"MulticastBuffer: {what} failed: {err}")
+            return res[1] if isinstance(res, tuple) and len(res) == 2 else res
+
+        fdtype = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        cudev = self._cudev = ok(cu.cuDeviceGet(self.device.index), "cuDeviceGet")
+        if ok(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cudev),
+              "cuDeviceGetAttribute") != 1:
+            raise RuntimeError("MulticastBuffer: the device has no multicast (NVLS) support")
+        self.half_bytes = -(-self.count * 8 // 256) * 256
+        self.flag_off = 2 * self.half_bytes
+        need = self.flag_off + 256
+        aprop = cu.CUmemAllocationProp()
+        aprop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        aprop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        aprop.location.id = self.device.index
+        aprop.requestedHandleTypes = fdtype
+        agran = ok(cu.cuMemGetAllocationGranularity(
+            aprop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "allocation granularity")
+        mprop = cu.CUmulticastObjectProp()
+        mprop.numDevices = self.world
+        mprop.handleTypes = fdtype
+        mprop.size = need
+        mgran = ok(cu.cuMulticastGetGranularity(
+            mprop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED), "multicast granularity")
+        gran = max(int(agran), int(mgran))
+        self.size = -(-need // gran) * gran
+        mprop.size = self.size
+        fd = None
+        if self.rank == 0:
+            self._mc = ok(cu.cuMulticastCreate(mprop), "cuMulticastCreate")
+            fd = ok(cu.cuMemExportToShareableHandle(self._mc, fdtype, 0), "export") if self.world > 1 else None
+        if self.world > 1:
+            fd_local = share_fd(fd, group)
+            if self.rank != 0:
+                self._mc = ok(cu.cuMemImportFromShareableHandle(fd_local, fdtype), "import")
+            os.close(fd_local)
+        ok(cu.cuMulticastAddDevice(self._mc, cudev), "cuMulticastAddDevice")
+        if self.world > 1:
+            dist.barrier(group=group)                  # every device added before any binding
+        self._mem = ok(cu.cuMemCreate(self.size, aprop, 0), "cuMemCreate")
+        ok(cu.cuMulticastBindMem(self._mc, 0, self._mem, 0, self.size, 0), "cuMulticastBindMem")
+        access = cu.CUmemAccessDesc()
+        access.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        access.location.id = self.device.index
+        access.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (unicast)"))
+        ok(cu.cuMemMap(self.uc, self.size, 0, self._mem, 0), "map (unicast)")
+        ok(cu.cuMemSetAccess(self.uc, self.size, [access], 1), "access (unicast)")
+        self.mc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (multicast)"))
+        ok(cu.cuMemMap(self.mc, self.size, 0, self._mc, 0), "map (multicast)")
+        ok(cu.cuMemSetAccess(self.mc, self.size, [access], 1), "access (multicast)")
+        ok(cu.cuMemsetD8(self.uc, 0, self.size), "zero")
+        ok(cu.cuCtxSynchronize(), "synchronize")
+        if self.world > 1:
+            dist.barrier(group=group)                  # every flag zeroed before any arrival
+        self.calls = 0
+
+    def step(self):
+        """Addresses for the next fs_allreduce_multicast_u64 call (see the class doc)."""
+        self.calls += 1
+        h = self.calls & 1
+        return (self.uc + h * self.half_bytes, self.mc + h * self.half_bytes, self.mc + self.flag_off,
+                self.uc + self.flag_off, (self.world * self.calls) & 0xFFFFFFFF)
+
+    def close(self):
+        cu = self._cu
+        if getattr(self, "_mem", None) is None:
+            return
+        torch.cuda.synchronize(self.device)
+        cu.cuMemUnmap(self.mc, self.size)
+        cu.cuMemUnmap(self.uc, self.size)
+        cu.cuMemAddressFree(self.mc, self.size)
+        cu.cuMemAddressFree(self.uc, self.size)
+        cu.cuMulticastUnbind(self._mc, self._cudev, 0, self.size)
+        cu.cuMemRelease(self._mem)
+        cu.cuMemRelease(self._mc)
+        self._mem = None
 
 
 def output_range(rank: int, world: int, n_total: int):
@@ -159,7 +315,9 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
     """Sort the union of all ranks' shards; returns (this rank's slice of the sorted
     output, (begin, end) global positions of that slice).  mode "P" writes into
     ``peers.buffers(...)`` (a PeerBuffers by default; pass one to reuse the
-    mappings across calls) and returns a view of this rank's buffer.
+    mappings across calls) and returns a view of this rank's buffer.  mode "N"
+    takes ``peers`` as a MulticastBuffer(65,664, device, group) (created on each
+    call if None; pass one to reuse it).
 
     Measurement hooks (bench.py): ``events`` -- a dict with CUDA events "x0" and
     "x1", recorded on the current stream around the payload exchange (modes A and
@@ -175,6 +333,18 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
     if mode == "B":
         prefix2 = ops.histogram_prefix_u16(shard)
         dist.all_reduce(prefix2, group=group)
+        n_total = int(prefix2[65536:].sum().item())
+        begin, end = output_range(rank, world, n_total)
+        return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)
+    if mode == "N":
+        if peers is None:
+            peers = MulticastBuffer(65536 + 128, dev, group)
+        uc_half, mc_half, flag_mc, flag_local, target = peers.step()
+        ops.histogram_prefix_u16_to(shard, uc_half)
+        prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
+        _mark(events, "x0")
+        ops.allreduce_multicast(mc_half, prefix2, flag_mc, flag_local, target)
+        _mark(events, "x1")
         n_total = int(prefix2[65536:].sum().item())
         begin, end = output_range(rank, world, n_total)
         return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)

@@ -6,7 +6,7 @@
 set -e
 cd "$(dirname "$0")/../.."
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-ALL="abi hist16 scan expand16 wide partition host_stream trie peer small16 exchange"
+ALL="abi hist16 scan expand16 wide partition host_stream trie peer small16 exchange nvls"
 SRCS="${VARSRC:-$ALL}"
 mkdir -p scripts/microbench/variants
 for spec in "$@"; do

@@ -76,6 +76,11 @@ V = ctypes.c_void_p
     lambda L: L.fs_get_item(None, V(0x3000), V(0x4000), 16, V(0x5000), 4, 0, V(0x6000), None),
     lambda L: L.fs_get_index(V(0x2000), V(0x3000), V(0x4000), 0, V(0x5000), 4, V(0x6000), None),
     lambda L: L.fs_hist_merge_u64(V(0x1000), None, V(0x3000), 4, None),
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, None, V(0x5000), 1, None),      # flag NULL
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, V(0x4002), V(0x5000), 1, None),  # flag align
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1004), V(0x9000), 4, V(0x4000), V(0x5000), 1, None),  # src align
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x1008), 4, V(0x4000), V(0x5000), 1, None),  # overlap
+    lambda L: L.fs_allreduce_multicast_u64(None, V(0x9000), 4, V(0x4000), V(0x5000), 1, None),       # src NULL
 ])
 def test_invalid_arguments_rejected_without_gpu(call):
     L = fs.lib()
@@ -113,3 +118,19 @@ def test_cpu_tensors_fail_loudly():
     import torch
     with pytest.raises(ValueError):
         fs.sort_keys(torch.zeros(10, dtype=torch.uint16))
+
+
+def test_multicast_allreduce_is_one_ldgmc_per_element():
+    """fs_allreduce_multicast_u64's kernel reads through the switch: its SASS holds
+    the multicast load-reduce (LDGMC ... ADD.64) and a system-scope RED for the
+    barrier (checked here, on CPU, because the pool's one-GPU boxes have no
+    NVSwitch multicast fabric to run it on: profiles/r02g/nvls_probe.txt)."""
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not on PATH")
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    fn = [blk for blk in sass.split("Function : ") if "k_allreduce_mc" in blk.split("\n", 1)[0]]
+    assert len(fn) == 1
+    assert "LDGMC.E.ADD.64" in fn[0]
+    assert "REDG.E.ADD.STRONG.SYS" in fn[0]

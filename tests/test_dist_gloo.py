@@ -82,6 +82,19 @@ class OracleOps:
     def synchronize(self, device):
         pass
 
+    # -- mode "N": the multicast buffer's halves live in FakeMulticast.store (keyed by
+    #    the local address); the switch's multimem.ld_reduce sum is an all_reduce
+    def histogram_prefix_u16_to(self, keys, out_ptr):
+        FakeMulticast.store[out_ptr] = self.histogram_prefix_u16(keys)
+
+    def allreduce_multicast(self, src_mc, dst, flag_mc, flag_local, target):
+        assert flag_mc == flag_local + FakeMulticast.MC, "flag: multicast and local views of one word"
+        assert target == dist.get_world_size() * FakeMulticast.calls, "target = G x calls on this flag"
+        t = FakeMulticast.store.pop(src_mc - FakeMulticast.MC).clone()
+        dist.all_reduce(t)
+        dst.copy_(t)
+        return dst
+
     def sort_pairs(self, keys, vals):
         import oracle
         k, v = oracle.sort_pairs_u64_u32(keys.numpy(), vals.numpy())
@@ -149,6 +162,24 @@ class _OracleExchange:
             dest_vals[dd].numpy()[slots] = self.v[order[sel]]
 
 
+class FakeMulticast:
+    """CPU stand-in of dist.MulticastBuffer: the same step() contract (two halves by
+    call parity, the flag's multicast/local addresses, target = G x calls) over
+    made-up addresses."""
+    MC = 1 << 40
+    store = {}
+    calls = 0
+
+    def __init__(self, world):
+        self.world = world
+
+    def step(self):
+        FakeMulticast.calls += 1
+        h = FakeMulticast.calls & 1
+        uc = 4096 + h * 65536 * 8
+        return uc, uc + self.MC, 3 * 65536 * 8 + self.MC, 3 * 65536 * 8, self.world * FakeMulticast.calls
+
+
 class SharedPeers:
     """CPU stand-in of dist.PeerBuffers: shared-memory buffers made by the parent."""
 
@@ -178,7 +209,7 @@ def shard_bounds(n_total, world, rank, uneven):
     return cuts[rank], cuts[rank + 1]
 
 
-CASES = [(mode, d, uneven) for mode in ("B", "A", "P")
+CASES = [(mode, d, uneven) for mode in ("B", "A", "P", "N")
          for d, uneven in (("uniform", False), ("zipf", True), ("const", False), ("sortedswap", True))]
 N_TOTAL = 50_003
 
@@ -190,12 +221,13 @@ def worker(rank, world, port, outdir, peer_bufs):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    mc = FakeMulticast(world)   # one buffer across the mode-N cases: the halves alternate
     try:
         for ci, (mode, dist_name, uneven) in enumerate(CASES):
             b, e = shard_bounds(N_TOTAL, world, rank, uneven)
             full = datagen.gen_u16(dist_name, N_TOTAL, seed=3)
             shard = torch.from_numpy(full[b:e].copy())
-            peers = SharedPeers(peer_bufs[ci]) if mode == "P" else None
+            peers = SharedPeers(peer_bufs[ci]) if mode == "P" else (mc if mode == "N" else None)
             out, (ob, oe) = fsdist.sort_keys_u16(shard, mode=mode, ops=OracleOps(), peers=peers)
             np.save(os.path.join(outdir, f"out_{ci}_{rank}.npy"), out.numpy())
             np.save(os.path.join(outdir, f"range_{ci}_{rank}.npy"), np.array([ob, oe], dtype=np.int64))
@@ -205,7 +237,8 @@ def worker(rank, world, port, outdir, peer_bufs):
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_distributed_sort_matches_oracle(tmp_path, world):
-    """Modes A, B and P (expand-to-peer), four distributions (uneven and empty shards included)."""
+    """Modes A, B, P (expand-to-peer) and N (NVLS orchestration, stand-in switch), four
+    distributions (uneven and empty shards included)."""
     import datagen
     import oracle
     cap = -(-N_TOTAL // world)
@@ -357,3 +390,30 @@ def test_splitter_levels_and_cuts_single_process(G, kind):
             part = perm[cuts_all[r][d]:cuts_all[r][d + 1]]
             assert np.all(owner_of[part] == d), (r, d)
             assert part.size == int((owner_of[cuts_in[r]:cuts_in[r + 1]] == d).sum())
+
+
+def _fd_worker(rank, world, port, path):
+    sys.path.insert(0, ROOT)
+    from paper_2605_10390_b200 import dist as fsdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fd = os.open(path, os.O_RDONLY) if rank == 0 else None
+        got = fsdist.share_fd(fd, None)
+        assert os.pread(got, 64, 0) == b"multicast handle stand-in"   # the same open file (shared offset: pread)
+        if rank:
+            assert got != fd
+        os.close(got)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_share_fd(tmp_path, world):
+    """dist.share_fd (how MulticastBuffer hands rank 0's POSIX multicast handle to
+    the other ranks): every rank ends up with a descriptor of rank 0's open file."""
+    path = tmp_path / "h"
+    path.write_bytes(b"multicast handle stand-in")
+    mp.start_processes(_fd_worker, args=(world, free_port(), str(path)), nprocs=world, join=True,
+                       start_method="spawn")

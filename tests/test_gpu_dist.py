@@ -168,3 +168,65 @@ def test_fused_pair_exchange_virtual_ranks(cuda, G, kind):
     np.testing.assert_array_equal(gv, ev)
     # the splitters are exactly the keys at the rank boundaries
     assert K == [int(ek[(n * d) // G]) for d in range(1, G)]
+
+
+# ---------------------------------------------------------------- mode "N": NVLS multicast
+@pytest.fixture(scope="module")
+def mcbuf(cuda, nccl_group):
+    from cuda.bindings import driver as cu
+    err, d = cu.cuDeviceGet(cuda.index)
+    err, mc_ok = cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d)
+    if mc_ok != 1:
+        pytest.skip("the device reports no multicast (NVLS) support")
+    try:
+        b = fsdist.MulticastBuffer(65536 + 128, cuda)
+    except RuntimeError as e:
+        # The pool's one-GPU boxes report multicast support but the driver refuses to
+        # create any multicast object (CUDA_ERROR_INVALID_VALUE for every size, handle
+        # type and device count, from C as well: GPU fabric GUID 0, no NVSwitch
+        # fabric in the slice; profiles/r02g/nvls_probe.txt).  Any other failure fails.
+        if "cuMulticastCreate failed" not in str(e):
+            raise
+        pytest.skip(f"no NVSwitch multicast fabric on this box: {e}")
+    yield b
+    b.close()
+
+
+def _to_raw(dst_ptr, t):
+    from cuda.bindings import driver as cu
+    torch.cuda.synchronize()
+    (err,) = cu.cuMemcpyDtoD(dst_ptr, t.data_ptr(), t.numel() * t.element_size())
+    assert err == cu.CUresult.CUDA_SUCCESS, err
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("count", [1, 1000, 65536 + 128])
+def test_allreduce_multicast_single_rank(cuda, mcbuf, count):
+    """fs_allreduce_multicast_u64 through the multicast mapping of a one-GPU
+    multicast group: every element comes back through multimem.ld_reduce equal
+    to what the rank wrote (the sum over one rank), on both halves, over several
+    calls (the flag's target grows by G = 1 per call); count = 0 is a pure barrier."""
+    import paper_2605_10390_b200 as fs
+    gen = torch.Generator().manual_seed(count)
+    for call in range(4):
+        src = torch.randint(-(1 << 62), 1 << 62, (count,), generator=gen, dtype=torch.int64).to(cuda)
+        uc, mc, fmc, fl, target = mcbuf.step()
+        _to_raw(uc, src)
+        dst = torch.full((count,), -1, dtype=torch.int64, device=cuda)
+        fs.allreduce_multicast_u64(mc, dst, fmc, fl, target)
+        torch.cuda.synchronize()
+        assert torch.equal(dst, src), (count, call)
+    uc, mc, fmc, fl, target = mcbuf.step()
+    fs.allreduce_multicast_u64(mc, torch.empty(0, dtype=torch.int64, device=cuda), fmc, fl, target)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dist_name", ["uniform", "zipf", "const", "sortedswap"])
+@pytest.mark.parametrize("n", [1_000_003, 1 << 22])
+def test_dist_single_rank_nvls(cuda, nccl_group, mcbuf, dist_name, n):
+    """Mode N (histogram prefix written into the multicast-bound buffer, summed by
+    the switch, own range expanded) on one rank equals the oracle sort."""
+    keys = datagen.gen_u16(dist_name, n, seed=5)
+    out, (b, e) = fsdist.sort_keys_u16(torch.from_numpy(keys).to(cuda), mode="N", peers=mcbuf)
+    assert (b, e) == (0, keys.size)
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.sort_u16(keys))
