@@ -91,6 +91,8 @@ static_assert(32768 + 255 + kThreads * kUnroll * 8 < 65536, "spill bound violate
 // The CTA's hot key (skewed inputs): the first key whose counter crossed 2^15
 // (0xFFFFFFFF: none yet).  Warps that see it count that key in registers.
 __shared__ uint32_t s_hot_key;
+// (A third hot word, redirected the same way, measured slower on Zipf: 258.6 ->
+// 283.1 us, 280.2 with FS_HIST_FMA 2; profiles/r02g/u16_variants_hot3.txt.)
 // FS_HIST_HOT2W: a second hot word (the first spill of another word once the
 // first is set), redirected to a second per-thread dummy.
 #ifndef FS_HIST_HOT2W
@@ -116,6 +118,37 @@ FS_DEVINL void add_key(uint32_t* sh, uint32_t k, uint32_t cnt, unsigned long lon
   if (old & kHotMask) spill_word(sh, w, spill);
 }
 
+// FS_HIST_FMA: the increments and the high key's shift computed on the FMA pipe
+// (IMAD / IMAD.HI) instead of the ALU pipe.  The ALU pipe is what saturates in
+// the redirecting (skewed-input) loop: its two compare + select pairs per key
+// come on top of the plain loop's address and increment arithmetic, and the
+// compiler turns (b * 0xFFFF + 1) into compare + select and max(.., 1) into
+// VIMNMX, all ALU (profiles/ncu_summary_r02f_c3a.md: math_pipe_throttle).
+// Zipf 265.7 -> 258.5 us per sort, other inputs unchanged; moving the masks
+// and bit extractions over as well (ALU:FMA 74:65 instead of 103:38 in the
+// redirecting block) gained nothing more (profiles/r02g/u16_variants_fma.txt).
+#ifndef FS_HIST_FMA
+#define FS_HIST_FMA 1
+#endif
+// b * 0xFFFF + 1 for a bit b: 1 or 0x10000 (one IMAD; opaque to the compiler's select rewrite)
+FS_DEVINL uint32_t inc_of_bit(uint32_t b) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, 65535, 1;" : "=r"(r) : "r"(b));
+  return r;
+}
+// x >> k as the high word of x * 2^(32 - k) (IMAD.HI)
+template <int k>
+FS_DEVINL uint32_t shr_hi(uint32_t x) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(1u << (32 - k)));
+  return r;
+}
+// Word byte offset and increment of the low / high key of a packed pair x.
+FS_DEVINL uint32_t addr_lo(uint32_t x) { return (x + x) & 0x1FFFCu; }
+FS_DEVINL uint32_t addr_hi(uint32_t x) { return (FS_HIST_FMA ? shr_hi<15>(x) : (x >> 15)) & 0x1FFFCu; }
+FS_DEVINL uint32_t inc_lo(uint32_t x) { return FS_HIST_FMA ? inc_of_bit(x & 1u) : (x & 1u) * 0xFFFFu + 1u; }
+FS_DEVINL uint32_t inc_hi(uint32_t x) { return FS_HIST_FMA ? inc_of_bit(shr_hi<16>(x) & 1u) : max(x & 0x10000u, 1u); }
+
 // 8 atomics; returns the OR of the old words.  Word byte offset of the low key
 // of x is (x & 0xFFFE) * 2, of the high key (x >> 17) * 4; the increment is 1 or
 // 0x10000 by the key's lowest bit.
@@ -126,8 +159,8 @@ FS_DEVINL uint32_t add8(uint32_t* sh, const uint4& v) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t x = w[j];
-    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x + x) & 0x1FFFCu)), (x & 1u) * 0xFFFFu + 1u);
-    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + ((x >> 15) & 0x1FFFCu)), max(x & 0x10000u, 1u));
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + addr_lo(x)), inc_lo(x));
+    acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + addr_hi(x)), inc_hi(x));
   }
   return acc;
 }
@@ -160,14 +193,14 @@ FS_DEVINL uint32_t add8_hot(uint32_t* sh, const uint4& v, uint32_t h, uint32_t& 
       // increment: the dummy's halves count keys 2w and 2w + 1 exactly as the
       // table's word would, so one word compare replaces key extraction,
       // compare, increment select and register count.
-      const uint32_t a0 = (x + x) & 0x1FFFCu, a1 = (x >> 15) & 0x1FFFCu;
+      const uint32_t a0 = addr_lo(x), a1 = addr_hi(x);
       uint32_t b0 = a0 == h ? dummy_off : a0, b1 = a1 == h ? dummy_off : a1;
       if (FS_HIST_HOT2W) {
         b0 = a0 == h2 ? dummy2_off : b0;
         b1 = a1 == h2 ? dummy2_off : b1;
       }
-      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b0), (x & 1u) * 0xFFFFu + 1u);
-      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b1), max(x & 0x10000u, 1u));
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b0), inc_lo(x));
+      acc |= atomicAdd(reinterpret_cast<uint32_t*>(base + b1), inc_hi(x));
     } else if (FS_HIST_REDIRECT) {
       const bool pl = (x & 0xFFFFu) == h, ph = (x >> 16) == h;
       hc += (uint32_t)pl + (uint32_t)ph;
