@@ -197,6 +197,7 @@ class MulticastBuffer:
         self._cu, self.count, self.group = cu, int(count), group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.device = torch.device(device)
+        self._mem = None
         torch.cuda.set_device(self.device)
         torch.cuda.synchronize(self.device)            # the primary context is current on this thread
 
@@ -206,58 +207,93 @@ class MulticastBuffer:
                 raise RuntimeError(f"MulticastBuffer: {what} failed: {err}")
             return res[1] if isinstance(res, tuple) and len(res) == 2 else res
 
+        def agreed(step):
+            """This rank's part of a setup step, then a MIN all-reduce of the success
+            flags: if any rank failed, every rank raises here (none is left waiting
+            in a later collective).  Doubles as the barrier between steps."""
+            err = None
+            try:
+                step()
+            except Exception as e:  # noqa: BLE001 -- re-raised below, after the agreement
+                err = e
+            if self.world > 1:
+                on_dev = dist.get_backend(group) == "nccl"
+                flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=self.device if on_dev else "cpu")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+                if err is None and int(flag.item()) == 0:
+                    raise RuntimeError("MulticastBuffer: another rank failed a setup step")
+            if err is not None:
+                raise err
+
         fdtype = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
-        cudev = self._cudev = ok(cu.cuDeviceGet(self.device.index), "cuDeviceGet")
-        if ok(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cudev),
-              "cuDeviceGetAttribute") != 1:
-            raise RuntimeError("MulticastBuffer: the device has no multicast (NVLS) support")
         self.half_bytes = -(-self.count * 8 // 256) * 256
         self.flag_off = 2 * self.half_bytes
         need = self.flag_off + 256
-        aprop = cu.CUmemAllocationProp()
-        aprop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
-        aprop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
-        aprop.location.id = self.device.index
-        aprop.requestedHandleTypes = fdtype
-        agran = ok(cu.cuMemGetAllocationGranularity(
-            aprop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "allocation granularity")
-        mprop = cu.CUmulticastObjectProp()
-        mprop.numDevices = self.world
-        mprop.handleTypes = fdtype
-        mprop.size = need
-        mgran = ok(cu.cuMulticastGetGranularity(
-            mprop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED), "multicast granularity")
-        gran = max(int(agran), int(mgran))
-        self.size = -(-need // gran) * gran
-        mprop.size = self.size
-        fd = None
-        if self.rank == 0:
-            self._mc = ok(cu.cuMulticastCreate(mprop), "cuMulticastCreate")
-            fd = ok(cu.cuMemExportToShareableHandle(self._mc, fdtype, 0), "export") if self.world > 1 else None
-        if self.world > 1:
-            fd_local = share_fd(fd, group)
+        st = {}
+
+        def query():
+            st["cudev"] = ok(cu.cuDeviceGet(self.device.index), "cuDeviceGet")
+            if ok(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED,
+                                          st["cudev"]), "cuDeviceGetAttribute") != 1:
+                raise RuntimeError("MulticastBuffer: the device has no multicast (NVLS) support")
+            aprop = cu.CUmemAllocationProp()
+            aprop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+            aprop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+            aprop.location.id = self.device.index
+            aprop.requestedHandleTypes = fdtype
+            agran = ok(cu.cuMemGetAllocationGranularity(
+                aprop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "granularity")
+            mprop = cu.CUmulticastObjectProp()
+            mprop.numDevices = self.world
+            mprop.handleTypes = fdtype
+            mprop.size = need
+            mgran = ok(cu.cuMulticastGetGranularity(
+                mprop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED), "multicast granularity")
+            st["gran"] = max(int(agran), int(mgran))
+            self.size = -(-need // st["gran"]) * st["gran"]
+            mprop.size = self.size
+            st["aprop"], st["mprop"] = aprop, mprop
+
+        def create():
+            st["fd"] = None
+            if self.rank == 0:
+                self._mc = ok(cu.cuMulticastCreate(st["mprop"]), "cuMulticastCreate")
+                if self.world > 1:
+                    st["fd"] = ok(cu.cuMemExportToShareableHandle(self._mc, fdtype, 0), "export")
+
+        def import_():
             if self.rank != 0:
-                self._mc = ok(cu.cuMemImportFromShareableHandle(fd_local, fdtype), "import")
-            os.close(fd_local)
-        ok(cu.cuMulticastAddDevice(self._mc, cudev), "cuMulticastAddDevice")
+                self._mc = ok(cu.cuMemImportFromShareableHandle(st["fd_local"], fdtype), "import")
+            os.close(st["fd_local"])
+
+        def add_device():
+            ok(cu.cuMulticastAddDevice(self._mc, st["cudev"]), "cuMulticastAddDevice")
+
+        def bind_and_map():
+            gran = st["gran"]
+            self._mem = ok(cu.cuMemCreate(self.size, st["aprop"], 0), "cuMemCreate")
+            ok(cu.cuMulticastBindMem(self._mc, 0, self._mem, 0, self.size, 0), "cuMulticastBindMem")
+            access = cu.CUmemAccessDesc()
+            access.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+            access.location.id = self.device.index
+            access.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+            self.uc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (unicast)"))
+            ok(cu.cuMemMap(self.uc, self.size, 0, self._mem, 0), "map (unicast)")
+            ok(cu.cuMemSetAccess(self.uc, self.size, [access], 1), "access (unicast)")
+            self.mc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (multicast)"))
+            ok(cu.cuMemMap(self.mc, self.size, 0, self._mc, 0), "map (multicast)")
+            ok(cu.cuMemSetAccess(self.mc, self.size, [access], 1), "access (multicast)")
+            ok(cu.cuMemsetD8(self.uc, 0, self.size), "zero")
+            ok(cu.cuCtxSynchronize(), "synchronize")
+
+        agreed(query)
+        agreed(create)
         if self.world > 1:
-            dist.barrier(group=group)                  # every device added before any binding
-        self._mem = ok(cu.cuMemCreate(self.size, aprop, 0), "cuMemCreate")
-        ok(cu.cuMulticastBindMem(self._mc, 0, self._mem, 0, self.size, 0), "cuMulticastBindMem")
-        access = cu.CUmemAccessDesc()
-        access.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
-        access.location.id = self.device.index
-        access.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
-        self.uc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (unicast)"))
-        ok(cu.cuMemMap(self.uc, self.size, 0, self._mem, 0), "map (unicast)")
-        ok(cu.cuMemSetAccess(self.uc, self.size, [access], 1), "access (unicast)")
-        self.mc = int(ok(cu.cuMemAddressReserve(self.size, gran, 0, 0), "reserve (multicast)"))
-        ok(cu.cuMemMap(self.mc, self.size, 0, self._mc, 0), "map (multicast)")
-        ok(cu.cuMemSetAccess(self.mc, self.size, [access], 1), "access (multicast)")
-        ok(cu.cuMemsetD8(self.uc, 0, self.size), "zero")
-        ok(cu.cuCtxSynchronize(), "synchronize")
-        if self.world > 1:
-            dist.barrier(group=group)                  # every flag zeroed before any arrival
+            st["fd_local"] = share_fd(st["fd"], group)
+            agreed(import_)
+        self._cudev = st["cudev"]
+        agreed(add_device)        # every device added before any binding
+        agreed(bind_and_map)      # every flag zeroed before any arrival
         self.calls = 0
 
     def step(self):
