@@ -230,12 +230,18 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm: shared helpers
-def load_traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the newest committed ncu capture."""
+def load_traffic(kernel: str, workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the newest committed ncu capture
+    of this workload (profiles/ncu_traffic_<round>_<workload>.json; before per-workload names,
+    profiles/ncu_traffic_<round>.json held the c2 / c5 kernels)."""
+    import re
     pdir = os.path.join(ROOT, "profiles")
     names = sorted(os.listdir(pdir), reverse=True) if os.path.isdir(pdir) else []
-    for name in names:
-        if name.startswith("ncu_traffic") and name.endswith(".json"):
+    own = [n for n in names if n.startswith("ncu_traffic") and n.endswith(f"_{workload}.json")]
+    legacy = [n for n in names if n.startswith("ncu_traffic") and n.endswith(".json")
+              and not re.search(r"_c\d[a-z]?\.json$", n)] if workload in ("c2", "c5") else []
+    for name in own + legacy:
+        if True:
             try:
                 d = json.load(open(os.path.join(pdir, name)))
                 if kernel in d:
@@ -438,7 +444,7 @@ def run_fs_pairs(args, dev):
     alg = metrics.minimal_bytes_pairs(n, 8, 4)  # each MSD pass moves every pair once: read + write
     achieved = alg / (phase[dom] * 1e-3) / 1e9
     method_b = 80 * n if path == "msd" else 200 * n
-    traffic, traffic_src = load_traffic(names[dom])
+    traffic, traffic_src = load_traffic(names[dom], "c5")
     line = {
         "metric": METRIC, "value": round(n * args.steps / (total_ms * 1e-3) / 1e9, 3), "unit": "Gkeys/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step, 4),
@@ -579,7 +585,7 @@ def run_fs(args, rank, world, local_rank):
     alg_bytes = 2 * (n if dom == "hist16" else (b1 - b0))
     peak, peak_src = measured_peak_gbs()
     achieved = alg_bytes / (names[dom] * 1e-3) / 1e9
-    traffic, traffic_src = load_traffic(dom) if (args.workload == "c2" and world == 1) else (None, None)
+    traffic, traffic_src = load_traffic(dom, args.workload) if world == 1 else (None, None)
     whole_bytes = metrics.minimal_bytes_keys(n, 2)  # the u16 sort reads and writes every key once
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
@@ -611,7 +617,7 @@ def run_fs(args, rank, world, local_rank):
                    "(launch-bound size)" if use_graph else ""),
     }
     if args.workload == "c2" and world == 1 and traffic is not None:
-        t_exp, _ = load_traffic("expand16")
+        t_exp, _ = load_traffic("expand16", "c2")
         if t_exp:
             line["b_eff"] = {"value": round(metrics.bandwidth_efficiency(whole_bytes, traffic + t_exp), 4),
                              "useful_bytes": whole_bytes,
