@@ -182,6 +182,17 @@ def share_fd(fd, group=None):
     return fds[0]
 
 
+def multicast_step(calls: int, world: int, uc: int, mc: int, half_bytes: int, flag_off: int):
+    """Call number ``calls`` (1, 2, ...) of fs_allreduce_multicast_u64 on a
+    MulticastBuffer: (local half, multicast half, flag multicast, flag local,
+    target).  Halves alternate by call parity, so a rank rewrites a half only two
+    calls after it was read (every rank has arrived at the call in between);
+    target = G x calls, the flag's value once every rank has arrived (mod 2^32:
+    the kernel compares wrap-safely)."""
+    h = calls & 1
+    return (uc + h * half_bytes, mc + h * half_bytes, mc + flag_off, uc + flag_off, (world * calls) & 0xFFFFFFFF)
+
+
 class MulticastBuffer:
     """``count`` u64 per half, two halves (alternated by call parity), and a u32
     flag, in every rank's GPU memory, all bound at the same offsets into ONE
@@ -299,9 +310,7 @@ class MulticastBuffer:
     def step(self):
         """Addresses for the next fs_allreduce_multicast_u64 call (see the class doc)."""
         self.calls += 1
-        h = self.calls & 1
-        return (self.uc + h * self.half_bytes, self.mc + h * self.half_bytes, self.mc + self.flag_off,
-                self.uc + self.flag_off, (self.world * self.calls) & 0xFFFFFFFF)
+        return multicast_step(self.calls, self.world, self.uc, self.mc, self.half_bytes, self.flag_off)
 
     def close(self):
         cu = self._cu

@@ -417,3 +417,21 @@ def test_share_fd(tmp_path, world):
     path.write_bytes(b"multicast handle stand-in")
     mp.start_processes(_fd_worker, args=(world, free_port(), str(path)), nprocs=world, join=True,
                        start_method="spawn")
+
+
+def test_multicast_step_contract():
+    """MulticastBuffer.step's addresses: the two halves alternate by call parity
+    (consecutive calls never share a half), the flag's multicast and local
+    addresses are the same offset in the two mappings, and the target is G x
+    calls modulo 2^32 (wrap-safe in the kernel)."""
+    from paper_2605_10390_b200.dist import multicast_step
+    uc, mc, half, flag = 0x7F0000000000, 0x7E0000000000, 525_312, 2 * 525_312
+    prev = None
+    for calls in range(1, 9):
+        u, m, fm, fl, tgt = multicast_step(calls, 8, uc, mc, half, flag)
+        assert u - uc == m - mc and (u - uc) in (0, half)
+        assert fm - mc == fl - uc == flag
+        assert tgt == 8 * calls
+        assert u != prev
+        prev = u
+    assert multicast_step(1 << 30, 8, uc, mc, half, flag)[4] == (8 << 30) & 0xFFFFFFFF
