@@ -292,13 +292,17 @@ fs_status fs_expand_to_peers_u16(const uint64_t* hist_all, int G, int g, uint64_
  * src_r is complete.  A caller that rewrites src before every rank has read it
  * must alternate two src regions by call parity.  All pointers device, 8-byte
  * (flags 4-byte) aligned; src_mc and dst must not overlap.  Every rank of the
- * multicast group must make the matching call, or the others wait forever (as
- * with any collective).  count = 0 still arrives and waits (a pure barrier).
- * Errors: FS_ERR_INVALID_ARGUMENT for NULL / misaligned / overlapping
- * arguments; FS_ERR_CUDA if the launch fails (e.g. src_mc not a multicast
- * mapping surfaces as an asynchronous fault at the caller's next sync). */
+ * multicast group must make the matching call; a rank whose peers have not all
+ * arrived within timeout_ns (0: wait forever) stops waiting, leaves dst
+ * unwritten and sets the device word *timed_out to 1 (callers zero it first and
+ * read it after synchronising).  count = 0 still arrives and waits (a pure
+ * barrier).  Errors: FS_ERR_INVALID_ARGUMENT for NULL / misaligned /
+ * overlapping arguments; FS_ERR_CUDA if the launch fails (e.g. src_mc not a
+ * multicast mapping surfaces as an asynchronous fault at the caller's next
+ * sync). */
 fs_status fs_allreduce_multicast_u64(const uint64_t* src_mc, uint64_t* dst, uint64_t count, uint32_t* flag_mc,
-                                     const uint32_t* flag_local, uint32_t target, fs_stream_t stream);
+                                     const uint32_t* flag_local, uint32_t target, uint64_t timeout_ns,
+                                     uint32_t* timed_out, fs_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use, and the out-of-core path of Batch

@@ -146,17 +146,25 @@ def histogram_prefix_u16(keys: torch.Tensor, prefix2: torch.Tensor | None = None
     return None if out_ptr is not None else prefix2
 
 
-def allreduce_multicast_u64(src_mc: int, dst: torch.Tensor, flag_mc: int, flag_local: int, target: int):
+def allreduce_multicast_u64(src_mc: int, dst: torch.Tensor, flag_mc: int, flag_local: int, target: int,
+                            timed_out: torch.Tensor | None = None, timeout_s: float = 60.0):
     """dst[i] = sum over ranks of their src[i] (int64/uint64 dst, i < dst.numel()), read through the
     multicast address src_mc by multimem.ld_reduce, with the call's cross-GPU barrier on the
-    flag word (fs_allreduce_multicast_u64; addresses from dist.MulticastBuffer)."""
+    flag word (fs_allreduce_multicast_u64; addresses from dist.MulticastBuffer).  ``timed_out``:
+    a device int32[1], zeroed here, set to 1 by the kernel if the peers did not all arrive within
+    ``timeout_s`` (dst is then not written); check it after synchronising.  Returns (dst, timed_out)."""
     dev = _require_cuda(dst)
     if dst.dtype not in (torch.int64, torch.uint64) or not dst.is_contiguous():
         raise TypeError("dst must be a contiguous 64-bit integer tensor")
+    if timed_out is None:
+        timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
+    else:
+        timed_out.zero_()
     with torch.cuda.device(dev):
         check(lib().fs_allreduce_multicast_u64(src_mc, dst.data_ptr(), dst.numel(), flag_mc, flag_local,
-                                               target & 0xFFFFFFFF, _stream(dev)), "fs_allreduce_multicast_u64")
-    return dst
+                                               target & 0xFFFFFFFF, int(timeout_s * 1e9), timed_out.data_ptr(),
+                                               _stream(dev)), "fs_allreduce_multicast_u64")
+    return dst, timed_out
 
 
 def expand_prefix_u16(prefix2: torch.Tensor, out_begin: int, out_end: int, out: torch.Tensor | None = None):

@@ -41,7 +41,7 @@ SIGNATURES = {
     "fs_bound_u64": (_i32, [_vp, _u64, _vp, _u64, _i32, _vp, _vp]),
     "fs_expand_to_peers_u16_temp_bytes": (_sz, [_u64, _i32]),
     "fs_expand_to_peers_u16": (_i32, [_vp, _i32, _i32, _u64, _vp, _vp, _sz, _vp]),
-    "fs_allreduce_multicast_u64": (_i32, [_vp, _vp, _u64, _vp, _vp, ctypes.c_uint32, _vp]),
+    "fs_allreduce_multicast_u64": (_i32, [_vp, _vp, _u64, _vp, _vp, ctypes.c_uint32, _u64, _vp, _vp]),
     "fs_trie_levels_count": (_sz, [_i32]),
     "fs_trie_levels": (_i32, [_vp, _i32, _vp, _vp]),
     "fs_trie_pack_words": (_sz, [_i32, _u64]),

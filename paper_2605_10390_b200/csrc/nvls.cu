@@ -46,16 +46,37 @@ FS_DEVINL uint32_t ld_acquire_sys_u32(const uint32_t* p) {
   return v;
 }
 
+FS_DEVINL uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kThreads)
     k_allreduce_mc(const uint64_t* __restrict__ src_mc, uint64_t* __restrict__ dst, uint64_t count,
-                   uint32_t* flag_mc, const uint32_t* flag_local, uint32_t target) {
+                   uint32_t* flag_mc, const uint32_t* flag_local, uint32_t target, uint64_t timeout_ns,
+                   uint32_t* timed_out) {
+  __shared__ uint32_t s_give_up;
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) mc_red_release_add_u32(flag_mc, 1u);
     // wrap-safe wait: every rank adds exactly G per call, so flag - target is a
-    // small negative number until all have arrived
-    while ((int32_t)(ld_acquire_sys_u32(flag_local) - target) < 0) __nanosleep(64);
+    // small negative number until all have arrived.  A rank that never arrives
+    // (a peer failed) must not hang this one: after timeout_ns the CTA gives up
+    // and reports it in *timed_out (dst is then not written).
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t give_up = 0;
+    while ((int32_t)(ld_acquire_sys_u32(flag_local) - target) < 0) {
+      __nanosleep(64);
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        give_up = 1;
+        atomicExch(timed_out, 1u);
+        break;
+      }
+    }
+    s_give_up = give_up;
   }
   __syncthreads();
+  if (s_give_up) return;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < count; i += stride)
     dst[i] = mc_ld_reduce_add_u64(src_mc + i);
@@ -68,9 +89,10 @@ using namespace fs;
 
 extern "C" fs_status fs_allreduce_multicast_u64(const uint64_t* src_mc, uint64_t* dst, uint64_t count,
                                                 uint32_t* flag_mc, const uint32_t* flag_local, uint32_t target,
-                                                fs_stream_t stream) {
+                                                uint64_t timeout_ns, uint32_t* timed_out, fs_stream_t stream) {
   FS_ENTRY();
-  if (!flag_mc || !flag_local) return fail(FS_ERR_INVALID_ARGUMENT, "NULL flag pointer");
+  if (!flag_mc || !flag_local || !timed_out) return fail(FS_ERR_INVALID_ARGUMENT, "NULL flag pointer");
+  if ((uintptr_t)timed_out & 3) return fail(FS_ERR_INVALID_ARGUMENT, "timed_out not 4-byte aligned");
   if (((uintptr_t)flag_mc | (uintptr_t)flag_local) & 3) return fail(FS_ERR_INVALID_ARGUMENT, "flag not 4-byte aligned");
   if (count > 0 && (!src_mc || !dst)) return fail(FS_ERR_INVALID_ARGUMENT, "NULL pointer with count > 0");
   if (((uintptr_t)src_mc | (uintptr_t)dst) & 7) return fail(FS_ERR_INVALID_ARGUMENT, "arrays not 8-byte aligned");
@@ -85,7 +107,8 @@ extern "C" fs_status fs_allreduce_multicast_u64(const uint64_t* src_mc, uint64_t
   // which arrives before it waits, so no co-residency is assumed
   const uint64_t want = (count + kThreads * 4 - 1) / (kThreads * 4);
   const unsigned grid = (unsigned)(want < 1 ? 1 : (want > (uint64_t)sms ? (uint64_t)sms : want));
-  k_allreduce_mc<<<grid, kThreads, 0, s>>>(src_mc, dst, count, flag_mc, flag_local, target);
+  k_allreduce_mc<<<grid, kThreads, 0, s>>>(src_mc, dst, count, flag_mc, flag_local, target,
+                                           timeout_ns ? timeout_ns : ~0ull, timed_out);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fs_allreduce_multicast_u64");
   return finish(s, "fs_allreduce_multicast_u64");
 }

@@ -113,7 +113,7 @@ class CudaOps:
 
     def allreduce_multicast(self, src_mc, dst, flag_mc, flag_local, target):
         from . import allreduce_multicast_u64
-        return allreduce_multicast_u64(src_mc, dst, flag_mc, flag_local, target)
+        return allreduce_multicast_u64(src_mc, dst, flag_mc, flag_local, target)   # (dst, timed_out flag)
 
     def synchronize(self, device):
         torch.cuda.synchronize(device)
@@ -161,6 +161,7 @@ def share_fd(fd, group=None):
         addr = "\0fractalsort-fd-" + uuid.uuid4().hex
         srv.bind(addr)
         srv.listen(world)
+        srv.settimeout(120)                                # a peer that never connects raises here, not a hang
         name = [addr]
     dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
     if rank == 0:
@@ -174,6 +175,7 @@ def share_fd(fd, group=None):
             srv.close()
         return fd
     with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.settimeout(120)
         c.connect(name[0])
         _, fds, _, _ = socket.recv_fds(c, 1, 1)
         c.sendall(b"k")
@@ -297,10 +299,13 @@ class MulticastBuffer:
             ok(cu.cuMemsetD8(self.uc, 0, self.size), "zero")
             ok(cu.cuCtxSynchronize(), "synchronize")
 
+        def share():
+            st["fd_local"] = share_fd(st["fd"], group)     # its socket steps time out instead of hanging
+
         agreed(query)
         agreed(create)
         if self.world > 1:
-            st["fd_local"] = share_fd(st["fd"], group)
+            agreed(share)
             agreed(import_)
         self._cudev = st["cudev"]
         agreed(add_device)        # every device added before any binding
@@ -388,9 +393,11 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         ops.histogram_prefix_u16_to(shard, uc_half)
         prefix2 = torch.empty(65536 + 128, dtype=torch.int64, device=dev)
         _mark(events, "x0")
-        ops.allreduce_multicast(mc_half, prefix2, flag_mc, flag_local, target)
+        _, timed_out = ops.allreduce_multicast(mc_half, prefix2, flag_mc, flag_local, target)
         _mark(events, "x1")
         n_total = int(prefix2[65536:].sum().item())
+        if int(timed_out.item()):
+            raise RuntimeError(f"mode N: rank {rank}: the other ranks did not reach the multicast all-reduce")
         begin, end = output_range(rank, world, n_total)
         return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)
     if mode == "A":

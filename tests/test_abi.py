@@ -76,11 +76,12 @@ V = ctypes.c_void_p
     lambda L: L.fs_get_item(None, V(0x3000), V(0x4000), 16, V(0x5000), 4, 0, V(0x6000), None),
     lambda L: L.fs_get_index(V(0x2000), V(0x3000), V(0x4000), 0, V(0x5000), 4, V(0x6000), None),
     lambda L: L.fs_hist_merge_u64(V(0x1000), None, V(0x3000), 4, None),
-    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, None, V(0x5000), 1, None),      # flag NULL
-    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, V(0x4002), V(0x5000), 1, None),  # flag align
-    lambda L: L.fs_allreduce_multicast_u64(V(0x1004), V(0x9000), 4, V(0x4000), V(0x5000), 1, None),  # src align
-    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x1008), 4, V(0x4000), V(0x5000), 1, None),  # overlap
-    lambda L: L.fs_allreduce_multicast_u64(None, V(0x9000), 4, V(0x4000), V(0x5000), 1, None),       # src NULL
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, None, V(0x5000), 1, 0, V(0x6000), None),  # flag
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, V(0x4002), V(0x5000), 1, 0, V(0x6000), None),
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1004), V(0x9000), 4, V(0x4000), V(0x5000), 1, 0, V(0x6000), None),
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x1008), 4, V(0x4000), V(0x5000), 1, 0, V(0x6000), None),
+    lambda L: L.fs_allreduce_multicast_u64(None, V(0x9000), 4, V(0x4000), V(0x5000), 1, 0, V(0x6000), None),
+    lambda L: L.fs_allreduce_multicast_u64(V(0x1000), V(0x9000), 4, V(0x4000), V(0x5000), 1, 0, None, None),  # timed_out
 ])
 def test_invalid_arguments_rejected_without_gpu(call):
     L = fs.lib()

@@ -213,12 +213,20 @@ def test_allreduce_multicast_single_rank(cuda, mcbuf, count):
         uc, mc, fmc, fl, target = mcbuf.step()
         _to_raw(uc, src)
         dst = torch.full((count,), -1, dtype=torch.int64, device=cuda)
-        fs.allreduce_multicast_u64(mc, dst, fmc, fl, target)
+        _, timed_out = fs.allreduce_multicast_u64(mc, dst, fmc, fl, target)
         torch.cuda.synchronize()
+        assert int(timed_out.item()) == 0
         assert torch.equal(dst, src), (count, call)
     uc, mc, fmc, fl, target = mcbuf.step()
-    fs.allreduce_multicast_u64(mc, torch.empty(0, dtype=torch.int64, device=cuda), fmc, fl, target)
+    _, timed_out = fs.allreduce_multicast_u64(mc, torch.empty(0, dtype=torch.int64, device=cuda), fmc, fl, target)
     torch.cuda.synchronize()
+    assert int(timed_out.item()) == 0
+    # a target no rank will reach (a missing peer): the call gives up after its timeout, dst untouched
+    uc, mc, fmc, fl, target = mcbuf.step()
+    dst = torch.full((count,), -1, dtype=torch.int64, device=cuda)
+    _, timed_out = fs.allreduce_multicast_u64(mc, dst, fmc, fl, target + 5, timeout_s=0.05)
+    torch.cuda.synchronize()
+    assert int(timed_out.item()) == 1 and bool((dst == -1).all())   # (the flag still counts this arrival: G x calls)
 
 
 @pytest.mark.parametrize("dist_name", ["uniform", "zipf", "const", "sortedswap"])
