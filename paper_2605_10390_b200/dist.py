@@ -318,6 +318,9 @@ class MulticastBuffer:
         return multicast_step(self.calls, self.world, self.uc, self.mc, self.half_bytes, self.flag_off)
 
     def close(self):
+        """Unmap and release this rank's memory and handle.  Other ranks read this
+        rank's memory through the switch: call it only once every rank's last
+        fs_allreduce_multicast_u64 on the buffer has completed (e.g. after a barrier)."""
         cu = self._cu
         if getattr(self, "_mem", None) is None:
             return
@@ -387,7 +390,8 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         begin, end = output_range(rank, world, n_total)
         return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)
     if mode == "N":
-        if peers is None:
+        own = peers is None                                    # a buffer made for this call is released after it
+        if own:
             peers = MulticastBuffer(65536 + 128, dev, group)
         uc_half, mc_half, flag_mc, flag_local, target = peers.step()
         ops.histogram_prefix_u16_to(shard, uc_half)
@@ -396,8 +400,12 @@ def sort_keys_u16(shard: torch.Tensor, group=None, mode: str = "B", ops=None, pe
         _, timed_out = ops.allreduce_multicast(mc_half, prefix2, flag_mc, flag_local, target)
         _mark(events, "x1")
         n_total = int(prefix2[65536:].sum().item())
-        if int(timed_out.item()):
+        if int(timed_out.item()):   # (a buffer made here is left mapped: a peer may still be reading it)
             raise RuntimeError(f"mode N: rank {rank}: the other ranks did not reach the multicast all-reduce")
+        if own:
+            if world > 1:
+                dist.barrier(group=group)                      # every rank's switch reads of this memory are done
+            peers.close()
         begin, end = output_range(rank, world, n_total)
         return ops.expand_prefix_u16(prefix2, begin, end), (begin, end)
     if mode == "A":
